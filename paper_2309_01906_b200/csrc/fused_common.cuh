@@ -1,0 +1,99 @@
+// fused_common.cuh — helpers shared by the fused (nest-shape specialised)
+// kernels: level-structure matching and the end-of-kernel combine climb.
+#pragma once
+#include "level_primitives.cuh"
+#include "plan.h"
+
+namespace hpar {
+
+// The device-visible levels of a nest (the host-applied GPU level dropped).
+struct LevelView {
+  int n;
+  const DevLevel* l[kMaxLev];
+  int idx[kMaxLev];
+};
+inline LevelView device_levels(const NestArgs& a) {
+  LevelView v;
+  v.n = 0;
+  for (int i = 0; i < a.nlev; ++i) {
+    if (a.lv[i].host_applied) continue;
+    v.l[v.n] = &a.lv[i];
+    v.idx[v.n] = i;
+    ++v.n;
+  }
+  return v;
+}
+// level bound to exactly one hardware level (lane: both lane slots)
+inline bool is_level(const DevLevel* L, int hw_slot) {
+  if (hw_slot == S_LANE) return L->sfirst == S_LANE && L->slast == S_LANE_IN;
+  return L->sfirst == hw_slot && L->slast == hw_slot;
+}
+
+// Write the partial of the task at `slot` to every nest level whose last
+// slot is `slot` (verify mode).  `index` = task id below the GPU.
+template <typename Acc>
+__device__ __forceinline__ void export_slot(const NestArgs& a, int slot, int64_t index, Acc v) {
+  if (!(a.verify & V_PARTIALS)) return;
+  for (int l = 0; l < a.nlev; ++l)
+    if (a.lv[l].slast == slot && a.partials[l]) ((Acc*)a.partials[l])[index] = v;
+}
+
+// Shared memory for the climb.
+template <typename Acc>
+struct ClimbSmem {
+  Acc warp[33];
+  Acc cta[16];
+  int flag;
+};
+
+// End-of-kernel TOTAL combine for the fused kernels (no lane partition):
+// lane -> warp (SHFL) -> CTA (smem, named barrier over the W consumer warps)
+// -> cluster (DSMEM + barrier.cluster) -> GPU (single-pass ticket).
+// Called by ALL threads of the CTA (consumers and any producer warp, which
+// passes the identity and is not part of the named barrier).  Writes the GPU
+// total to a.out and resets the ticket.  `W` = consumer warps.
+template <int OP, typename Acc>
+__device__ void fused_total_climb(const NestArgs& a, Acc v, int W, ClimbSmem<Acc>& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool consumer = warp < W;
+  const uint32_t rank = cluster_ctarank();
+  const int64_t cl = blockIdx.x / a.K;
+  if (consumer) {
+    export_slot<Acc>(a, S_LANE_IN, (int64_t)blockIdx.x * W * 32 + threadIdx.x, v);
+    v = warp_fold<OP>(v);
+    if (lane == 0) {
+      sh.warp[warp] = v;
+      export_slot<Acc>(a, S_WARP, (int64_t)blockIdx.x * W + warp, v);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(W * 32) : "memory");
+    if (threadIdx.x == 0) {
+      Acc r = OpT<OP, Acc>::identity();
+      for (int w = 0; w < W; ++w) r = OpT<OP, Acc>::combine(r, sh.warp[w]);
+      v = r;
+      export_slot<Acc>(a, S_CTA, (int64_t)blockIdx.x, v);
+      union { Acc x; unsigned long long u; } cv;
+      cv.x = v;
+      st_cluster_u64(mapa(smem_addr(&sh.cta[rank]), 0), cv.u);
+    }
+  }
+  cluster_sync_all();
+  Acc cluster_v = OpT<OP, Acc>::identity();
+  if (rank == 0 && threadIdx.x == 0) {
+    for (int k = 0; k < a.K; ++k) cluster_v = OpT<OP, Acc>::combine(cluster_v, sh.cta[k]);
+    export_slot<Acc>(a, S_CLUSTER, cl, cluster_v);
+  }
+  if (rank == 0) {
+    Acc* parts = (Acc*)a.cluster_partials;
+    if (grid_arrive<Acc>(cluster_v, parts, a.grid_ticket, cl, a.C, &sh.flag)) {
+      Acc tot = block_fold_ordered<OP, Acc>(parts, a.C, sh.warp);
+      if (threadIdx.x == 0) {
+        *(Acc*)a.out = tot;
+        export_slot<Acc>(a, S_GPU, 0, tot);
+        *a.grid_ticket = 0u;
+      }
+    }
+  }
+  cluster_sync_all();  // keep the leader's shared memory alive for its siblings
+}
+
+}  // namespace hpar

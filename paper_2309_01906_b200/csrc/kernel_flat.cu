@@ -1,0 +1,231 @@
+// kernel_flat.cu — fused flat nest reduction (configs 1 (flat form), 5).
+//
+// The nest shape it implements (the coalesced default):
+//     GPU      static            (host: rank shard, §8(a) A2)
+//     cluster  static(K*tile)    over the GPU's list
+//     CTA      static(tile)      over the cluster's list
+//     warp     static(32*V)      over the CTA's list        (V = 4 elements = 16 B)
+//     lane     static(V)         over the warp's list
+// Composed, CTA b = c*K + k owns global tiles  m*(C*K) + b  (m = 0, 1, ...)
+// and lane l of warp w reads, inside each tile, the 16-byte vectors
+// (r*W + w)*32 + l: exactly the owner map the oracle computes for this nest.
+//
+// B200 design: persistent grid of C clusters x K CTAs; one producer warp per
+// CTA streams the CTA's tiles with 1-D TMA bulk copies (cp.async.bulk,
+// L2 evict-first) into an S-stage shared-memory ring guarded by full/empty
+// mbarriers; W consumer warps read their vectors with LDS.128 and accumulate
+// (fp32 pairwise inside a vector, fp64 across vectors: §8(c) reading #6).
+// The lane -> warp -> CTA -> cluster -> GPU combine runs once at the end
+// (fused_common.cuh).  No GPU-scope fence inside the stream loop.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <type_traits>
+#include "fused_common.cuh"
+
+namespace hpar {
+namespace {
+
+constexpr int kStages = 4;
+
+template <typename In, typename Acc, int OP, bool VERIFY>
+__global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant__ NestArgs a, int W,
+                                                            int tile) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ ClimbSmem<Acc> csm;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n = a.n0;
+  const int64_t ntiles = (n + tile - 1) / tile;
+  const int64_t nblocks = (int64_t)gridDim.x;
+  const int64_t b = blockIdx.x;
+  const int64_t my_tiles = (b < ntiles) ? (ntiles - 1 - b) / nblocks + 1 : 0;
+  const In* x = (const In*)a.in;
+  const uint32_t tile_bytes = (uint32_t)tile * sizeof(In);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], W);
+    }
+    fence_mbarrier_init_cluster();
+  }
+  __syncthreads();
+
+  Acc acc = OpT<OP, Acc>::identity();
+  if (warp == W) {
+    // ---------------- producer warp: TMA bulk stream of the CTA's tiles ----
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int64_t j = 0; j < my_tiles; ++j) {
+        const int s = (int)(j % kStages);
+        if (j >= kStages) mbar_wait(&empty[s], (uint32_t)(((j / kStages) - 1) & 1));
+        const int64_t t = j * nblocks + b;
+        const int64_t base = t * tile;
+        const int64_t len = (n - base < tile) ? (n - base) : tile;
+        const uint32_t bytes = (uint32_t)((len * sizeof(In)) & ~(int64_t)15);  // TMA: multiple of 16 B
+        mbar_arrive_expect_tx(&full[s], bytes);
+        if (bytes) bulk_g2s(dsm + (size_t)s * tile_bytes, x + base, bytes, &full[s], pol);
+      }
+    }
+  } else {
+    // ---------------- W consumer warps ----------------------------------
+    const int vec_per_tile = tile / 4;
+    const int64_t leaf = (int64_t)a.rank * a.threads_per_gpu + b * W * 32 + threadIdx.x;
+    unsigned long long fpo = 0, fpw = 0, fpn = 0;
+    for (int64_t j = 0; j < my_tiles; ++j) {
+      const int s = (int)(j % kStages);
+      const int64_t t = j * nblocks + b;
+      const int64_t base = t * tile;
+      const int64_t len = (n - base < tile) ? (n - base) : tile;
+      mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
+      const In* st = (const In*)(dsm + (size_t)s * tile_bytes);
+      if (len == tile) {
+        if constexpr (sizeof(In) == 4) {
+#pragma unroll 4
+          for (int f = warp * 32 + lane; f < vec_per_tile; f += W * 32) {
+            if constexpr (OP == OP_SUM) {
+              if constexpr (std::is_floating_point<Acc>::value) {  // fp32 pairwise, then fp64
+                const float4 v = ((const float4*)st)[f];
+                acc += (double)((v.x + v.y) + (v.z + v.w));
+              } else {
+                const int4 v = ((const int4*)st)[f];
+                acc += (long long)v.x + (long long)v.y + (long long)v.z + (long long)v.w;
+              }
+            } else {
+              const In* e = st + 4 * f;
+              acc = OpT<OP, Acc>::combine(acc, (Acc)e[0]);
+              acc = OpT<OP, Acc>::combine(acc, (Acc)e[1]);
+              acc = OpT<OP, Acc>::combine(acc, (Acc)e[2]);
+              acc = OpT<OP, Acc>::combine(acc, (Acc)e[3]);
+            }
+            if constexpr (VERIFY) {
+              for (int q = 0; q < 4; ++q) {
+                const int64_t it = base + 4 * f + q;
+                if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
+                if (a.verify & V_FINGERPRINT) {
+                  const uint64_t g = a.global_begin + (uint64_t)it;
+                  fpo += fp_mix(g); fpw += fp_mix2(g, (uint64_t)leaf); fpn += 1;
+                }
+              }
+            }
+          }
+        }
+      } else {
+        // ragged last tile: bulk part from smem, the < 16 B tail from global
+        const int64_t in_smem = (len * (int64_t)sizeof(In)) / 16 * 16 / (int64_t)sizeof(In);
+        for (int f = warp * 32 + lane; f < vec_per_tile; f += W * 32) {
+          for (int q = 0; q < 4; ++q) {
+            const int64_t off = 4 * (int64_t)f + q;
+            if (off >= len) break;
+            const In e = (off < in_smem) ? st[off] : x[base + off];
+            acc = OpT<OP, Acc>::combine(acc, (Acc)e);
+            if constexpr (VERIFY) {
+              const int64_t it = base + off;
+              if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
+              if (a.verify & V_FINGERPRINT) {
+                const uint64_t g = a.global_begin + (uint64_t)it;
+                fpo += fp_mix(g); fpw += fp_mix2(g, (uint64_t)leaf); fpn += 1;
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if constexpr (VERIFY) {
+      if (a.verify & V_FINGERPRINT) {
+        atomicAdd(&a.fp[0], fpo);
+        atomicAdd(&a.fp[1], fpw);
+        atomicAdd(&a.fp[2], fpn);
+      }
+    }
+  }
+  __syncwarp();
+  fused_total_climb<OP, Acc>(a, acc, W, csm);
+}
+
+int g_flat_tile = 4096;
+
+template <typename In, typename Acc, int OP, bool VERIFY>
+cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
+  auto kern = flat_tma_kernel<In, Acc, OP, VERIFY>;
+  const size_t smem = (size_t)kStages * tile * sizeof(In);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.C * a.K));
+  cfg.blockDim = dim3((unsigned)((W + 1) * 32));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)a.K;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, W, tile);
+}
+
+template <typename In, typename Acc, int OP>
+cudaError_t launch_v(const NestArgs& a, int W, int tile, cudaStream_t s) {
+  return a.verify ? launch_t<In, Acc, OP, true>(a, W, tile, s) : launch_t<In, Acc, OP, false>(a, W, tile, s);
+}
+
+}  // namespace
+
+// Does the nest have the coalesced flat shape (and the call suit the kernel)?
+bool flat_matches(const NestArgs& a, const char** why) {
+  if (a.nloops != 1 || a.keyed) { *why = "not a flat total"; return false; }
+  if (a.op == OP_HIST) { *why = "hist"; return false; }
+  if (a.in_dtype != DT_F32 && a.in_dtype != DT_I32) { *why = "dtype"; return false; }
+  if (((uintptr_t)a.in & 15) != 0) { *why = "input not 16-byte aligned"; return false; }
+  if (a.lane_w != 1) { *why = "lane partition"; return false; }
+  LevelView v = device_levels(a);
+  if (v.n != 4) { *why = "needs cluster, CTA, warp, lane levels"; return false; }
+  const DevLevel *c = v.l[0], *k = v.l[1], *w = v.l[2], *l = v.l[3];
+  if (!is_level(c, S_CLUSTER) || !is_level(k, S_CTA) || !is_level(w, S_WARP) || !is_level(l, S_LANE)) {
+    *why = "levels not cluster/CTA/warp/lane";
+    return false;
+  }
+  const int64_t W = a.radix[S_WARP];
+  const int64_t tile = k->chunk;
+  if (l->sched != SCHED_STATIC_CHUNK || l->chunk != 4) { *why = "lane must be static(4)"; return false; }
+  if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 128) { *why = "warp must be static(128)"; return false; }
+  if (k->sched != SCHED_STATIC_CHUNK || tile % (128 * W) != 0 || tile * 4 > 32768) {
+    *why = "CTA must be static(tile), tile a multiple of 128*W, <= 32 KiB";
+    return false;
+  }
+  if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster must be static(K*tile)"; return false; }
+  if (W > 31) { *why = "W > 31 (one producer warp is added)"; return false; }
+  return true;
+}
+
+cudaError_t launch_flat(const NestArgs& a, int W, cudaStream_t s, const char** name) {
+  const LevelView v = device_levels(a);
+  const int tile = (int)v.l[1]->chunk;
+  *name = "flat_tma";
+  if (a.in_dtype == DT_F32) {
+    if (a.op == OP_SUM) return launch_v<float, double, OP_SUM>(a, W, tile, s);
+    if (a.op == OP_MIN) return launch_v<float, double, OP_MIN>(a, W, tile, s);
+    if (a.op == OP_MAX) return launch_v<float, double, OP_MAX>(a, W, tile, s);
+  } else {
+    if (a.op == OP_SUM) return launch_v<int32_t, long long, OP_SUM>(a, W, tile, s);
+    if (a.op == OP_MIN) return launch_v<int32_t, long long, OP_MIN>(a, W, tile, s);
+    if (a.op == OP_MAX) return launch_v<int32_t, long long, OP_MAX>(a, W, tile, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int flat_resident_ctas_per_sm(int W) {
+  int n = 0;
+  auto kern = flat_tma_kernel<float, double, OP_SUM, false>;
+  const size_t smem = (size_t)kStages * g_flat_tile * 4;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 2;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, (W + 1) * 32, smem) != cudaSuccess || n < 1) return 2;
+  return n;
+}
+
+}  // namespace hpar

@@ -1,0 +1,766 @@
+// runtime.cpp — host side of libhpar.so: the C ABI of include/hpar.h.
+//
+//  * level table (Table 2 for B200; §8(a) A0)
+//  * nest validation and resolution (§8(a) A1)
+//  * planner: picks the kernel specialisation for a call, builds NestArgs
+//  * workspace (self-resetting tickets, cluster partials)
+//  * node level: one ncclAllReduce over NVLink on the caller's stream
+//    (§8(a) A9), NCCL resolved with dlopen from the library torch loaded
+//  * level barriers (§8(a) A10)
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+
+#include "hpar.h"
+#include "nccl.h"  // types only; functions are resolved with dlsym
+#include "plan.h"
+
+namespace hpar {
+cudaError_t launch_generic(const NestArgs& a, int threads, cudaStream_t s);
+cudaError_t launch_probe(int level, int64_t C, int K, int W, int rounds, unsigned long long* mismatches,
+                         cudaStream_t s);
+// fused specialisations (kernel_flat.cu, kernel_rowwise.cu, kernel_hist.cu)
+bool flat_matches(const NestArgs& a, const char** why);
+cudaError_t launch_flat(const NestArgs& a, int W, cudaStream_t s, const char** name);
+bool rowwise_matches(const NestArgs& a, const char** why);
+cudaError_t launch_rowwise(const NestArgs& a, int W, cudaStream_t s, const char** name);
+bool hist_matches(const NestArgs& a, const char** why);
+cudaError_t launch_hist(const NestArgs& a, int W, cudaStream_t s, const char** name);
+int flat_resident_ctas_per_sm(int W);
+}  // namespace hpar
+
+using namespace hpar;
+
+// ------------------------------------------------------------- errors ----
+static thread_local std::string g_last_error;
+
+static hpar_status fail(hpar_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+static hpar_status ok() {
+  g_last_error.clear();
+  return HPAR_OK;
+}
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) return fail(HPAR_E_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+extern "C" const char* hpar_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char* hpar_version(void) { return "hpar 0.1 (sm_100a)"; }
+
+// --------------------------------------------------------------- NCCL ----
+namespace {
+struct NcclApi {
+  bool loaded = false;
+  std::string why;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+      nullptr;
+  ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*commUserRank)(const ncclComm_t, int*) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  const char* (*getLastError)(ncclComm_t) = nullptr;
+};
+NcclApi g_nccl;
+std::once_flag g_nccl_once;
+
+void load_nccl() {
+  // Prefer the NCCL already loaded into the process (torch's), so a
+  // communicator borrowed from torch's ProcessGroupNCCL is ABI-compatible.
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    g_nccl.why = dlerror() ? dlerror() : "dlopen(libnccl.so.2) failed";
+    return;
+  }
+  g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.commCount = (decltype(g_nccl.commCount))dlsym(h, "ncclCommCount");
+  g_nccl.commUserRank = (decltype(g_nccl.commUserRank))dlsym(h, "ncclCommUserRank");
+  g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.getLastError = (decltype(g_nccl.getLastError))dlsym(h, "ncclGetLastError");
+  g_nccl.loaded = g_nccl.allReduce && g_nccl.commCount && g_nccl.commUserRank && g_nccl.getErrorString;
+  if (!g_nccl.loaded) g_nccl.why = "libnccl.so.2 lacks required symbols";
+}
+hpar_status need_nccl() {
+  std::call_once(g_nccl_once, load_nccl);
+  if (!g_nccl.loaded) return fail(HPAR_E_NCCL, "NCCL unavailable: %s", g_nccl.why.c_str());
+  return HPAR_OK;
+}
+hpar_status nccl_fail(ncclResult_t r, ncclComm_t comm, const char* what) {
+  const char* last = (g_nccl.getLastError && comm) ? g_nccl.getLastError(comm) : "";
+  return fail(HPAR_E_NCCL, "%s: %s %s", what, g_nccl.getErrorString(r), last ? last : "");
+}
+}  // namespace
+
+// --------------------------------------------------------- level table ----
+namespace {
+const char* kLevelNames[HPAR_NLEVELS] = {"node", "gpu", "cluster", "cta", "warp", "lane"};
+
+// Table 2 flags of the SIBLINGS at each hardware level (member convention,
+// §8 reading #1; per-level evidence in DESIGN.md "Level table").
+uint32_t level_props(int level) {
+  switch (level) {
+    case HPAR_NODE:
+      return HPAR_P_PROGRESS | HPAR_P_GROUPMEM;
+    case HPAR_GPU:  // NCCL rendezvous; no cross-GPU atomics; separate HBM
+      return HPAR_P_BARRIER | HPAR_P_PROGRESS | HPAR_P_GROUPMEM;
+    case HPAR_CLUSTER:  // no barrier (read "does not"), no co-residency guarantee
+      return HPAR_P_ATOMIC | HPAR_P_OVERSUB | HPAR_P_DYNAMIC | HPAR_P_GLOBALMEM | HPAR_P_GROUPMEM | HPAR_P_CACHE;
+    case HPAR_CTA:  // barrier.cluster, DSMEM, co-scheduled
+      return HPAR_P_BARRIER | HPAR_P_ATOMIC | HPAR_P_DYNAMIC | HPAR_P_PROGRESS | HPAR_P_GLOBALMEM |
+             HPAR_P_LOCALMEM | HPAR_P_GROUPMEM | HPAR_P_CACHE;
+    case HPAR_WARP:  // bar.sync, shared memory of the SM
+      return HPAR_P_BARRIER | HPAR_P_ATOMIC | HPAR_P_DYNAMIC | HPAR_P_PROGRESS | HPAR_P_GLOBALMEM |
+             HPAR_P_LOCALMEM | HPAR_P_CACHE;
+    case HPAR_LANE:  // __syncwarp, SHFL; independent thread scheduling: not lockstep
+      return HPAR_P_BARRIER | HPAR_P_SHUFFLE | HPAR_P_PROGRESS | HPAR_P_GLOBALMEM | HPAR_P_GROUPMEM | HPAR_P_CACHE;
+  }
+  return 0;
+}
+
+// Grainedness: the SM-cycle cost of one combine/barrier step among
+// the level's siblings (B300_MICROARCH measured constants).
+double level_grain(int level) {
+  switch (level) {
+    case HPAR_NODE: return 1e6;
+    case HPAR_GPU: return 2e4;     // NCCL small allreduce ~10 us
+    case HPAR_CLUSTER: return 5e3; // kernel boundary / single pass through L2
+    case HPAR_CTA: return 380;     // barrier.cluster
+    case HPAR_WARP: return 47;     // named bar.sync
+    case HPAR_LANE: return 30;     // SHFL
+  }
+  return 1;
+}
+
+int64_t default_resident_clusters(const hpar_device_desc& d, int K, int W) {
+  int threads = W * 32;
+  int by_threads = d.max_threads_per_sm / std::max(threads, 1);
+  int per_sm = std::min(std::max(by_threads, 1), std::max(d.max_blocks_per_sm, 1));
+  per_sm = std::min(per_sm, 4);  // the fused streaming kernels' residency
+  int64_t ctas = (int64_t)d.sm_count * per_sm;
+  return std::max<int64_t>(1, ctas / std::max(K, 1));
+}
+}  // namespace
+
+extern "C" hpar_status hpar_device_describe(int32_t device, hpar_device_desc* out) {
+  if (!out) return fail(HPAR_E_INVALID, "hpar_device_describe: out is NULL");
+  cudaDeviceProp p;
+  CUDA_TRY(cudaGetDeviceProperties(&p, device));
+  memset(out, 0, sizeof(*out));
+  out->sm_count = p.multiProcessorCount;
+  out->max_threads_per_sm = p.maxThreadsPerMultiProcessor;
+  out->max_blocks_per_sm = p.maxBlocksPerMultiProcessor;
+  out->warp_size = p.warpSize;
+  out->smem_per_block_optin = (int64_t)p.sharedMemPerBlockOptin;
+  out->smem_per_sm = (int64_t)p.sharedMemPerMultiprocessor;
+  out->l2_bytes = p.l2CacheSize;
+  out->hbm_bytes = (int64_t)p.totalGlobalMem;
+  out->cc_major = p.major;
+  out->cc_minor = p.minor;
+  int cl = 0;
+  cudaDeviceGetAttribute(&cl, cudaDevAttrClusterLaunch, device);
+  out->cluster_launch = cl;
+  out->max_cluster_size = 8;
+  return ok();
+}
+
+extern "C" hpar_status hpar_hierarchy_describe(const hpar_device_desc* d, int32_t nranks, int32_t cluster_dim,
+                                               int32_t warps_per_cta, int64_t clusters,
+                                               hpar_level_info out[HPAR_NLEVELS], int32_t* nlevels) {
+  if (!d || !out) return fail(HPAR_E_INVALID, "hpar_hierarchy_describe: NULL argument");
+  if (nranks < 1) return fail(HPAR_E_INVALID, "nranks must be >= 1");
+  const int K = cluster_dim > 0 ? cluster_dim : 2;
+  const int W = warps_per_cta > 0 ? warps_per_cta : 8;
+  const int64_t C = clusters > 0 ? clusters : default_resident_clusters(*d, K, W);
+  const int64_t num[HPAR_NLEVELS] = {1, nranks, C, K, W, 32};
+  const int64_t maxn[HPAR_NLEVELS] = {1, nranks, (int64_t)0x7FFFFFFF / K, 16, 32, 32};
+  const uint64_t smem = (uint64_t)d->smem_per_block_optin;
+  const uint64_t localmem[HPAR_NLEVELS] = {0, 0, 0, (uint64_t)K * smem, smem, 0};
+  const uint64_t groupmem[HPAR_NLEVELS] = {0, (uint64_t)d->hbm_bytes, (uint64_t)K * smem, smem, 0, 255 * 4};
+  for (int l = 0; l < HPAR_NLEVELS; ++l) {
+    hpar_level_info& r = out[l];
+    memset(&r, 0, sizeof(r));
+    r.level = l;
+    r.props = level_props(l);
+    strncpy(r.name, kLevelNames[l], sizeof(r.name) - 1);
+    r.num = num[l];
+    r.max_num = maxn[l];
+    r.localmem_bytes = localmem[l];
+    r.groupmem_bytes = groupmem[l];
+    r.grainedness = level_grain(l);
+  }
+  if (nlevels) *nlevels = HPAR_NLEVELS;
+  return ok();
+}
+
+extern "C" hpar_status hpar_hierarchy_query(int32_t device, void* nccl_comm, hpar_level_info out[HPAR_NLEVELS],
+                                            int32_t* nlevels) {
+  hpar_device_desc d;
+  hpar_status s = hpar_device_describe(device, &d);
+  if (s) return s;
+  int nranks = 1;
+  if (nccl_comm) {
+    if ((s = need_nccl())) return s;
+    ncclResult_t r = g_nccl.commCount((ncclComm_t)nccl_comm, &nranks);
+    if (r != ncclSuccess) return nccl_fail(r, (ncclComm_t)nccl_comm, "ncclCommCount");
+  }
+  CUDA_TRY(cudaSetDevice(device));
+  const int K = 2, W = 8;
+  int64_t C = (int64_t)d.sm_count * hpar::flat_resident_ctas_per_sm(W) / K;
+  return hpar_hierarchy_describe(&d, nranks, K, W, C, out, nlevels);
+}
+
+// --------------------------------------------------------------- nests ----
+struct hpar_nest {
+  hpar_nest_config cfg;
+  int32_t device;
+  int32_t rank, nranks;
+  void* comm;
+  int nlev;
+  hpar_nest_level user[HPAR_MAX_NEST];
+  DevLevel lv[HPAR_MAX_NEST];
+  uint32_t props[HPAR_MAX_NEST];
+  int64_t radix[S_NSLOTS];
+  int lane_w;
+  bool lane_part = false;
+  int64_t G, C, K, W;
+  int gpu_level;  // nest level holding the GPU slot, or -1
+  // workspace
+  unsigned int* grid_ticket = nullptr;
+  void* cluster_partials = nullptr;
+  size_t cluster_partials_bytes = 0;
+  unsigned long long* dyn_tickets = nullptr;
+  int64_t dyn_slots = 0;
+  int32_t* error_flag = nullptr;
+  int* barrier_word = nullptr;
+  std::string last_kernel = "none";
+};
+
+namespace {
+// slot range of a hardware level range, given whether `first` is the inner
+// slice of a lane partition carried from the previous nest level and whether
+// `last` is partitioned here.
+int slot_first(int hw, bool inner_slice) {
+  if (hw == HPAR_LANE) return inner_slice ? S_LANE_IN : S_LANE;
+  return hw - 1;  // GPU=1 -> 0, CLUSTER -> 1, CTA -> 2, WARP -> 3
+}
+int slot_last(int hw, bool partitioned) {
+  if (hw == HPAR_LANE) return partitioned ? S_LANE : S_LANE_IN;
+  return hw - 1;
+}
+const char* sched_name(int s) {
+  static const char* n[] = {"static", "static(c)", "dynamic(c)", "none"};
+  return (s >= 0 && s < 4) ? n[s] : "?";
+}
+}  // namespace
+
+extern "C" hpar_status hpar_nest_create(const hpar_nest_level* lv, int32_t nlevels, const hpar_nest_config* cfg,
+                                        hpar_nest_t* out) {
+  if (!lv || !cfg || !out) return fail(HPAR_E_INVALID, "hpar_nest_create: NULL argument");
+  *out = nullptr;
+  if (nlevels < 1 || nlevels > HPAR_MAX_NEST)
+    return fail(HPAR_E_INVALID, "nest must have 1..%d levels (got %d)", HPAR_MAX_NEST, nlevels);
+  const bool describe_only = cfg->device < 0;
+  if (describe_only && !cfg->desc) return fail(HPAR_E_INVALID, "describe-only nest (device -1) needs cfg->desc");
+
+  hpar_nest* n = new hpar_nest();
+  n->cfg = *cfg;
+  n->device = cfg->device;
+  n->nlev = nlevels;
+  n->comm = cfg->nccl_comm;
+  n->rank = cfg->rank;
+  n->nranks = cfg->nranks > 0 ? cfg->nranks : 1;
+  auto bail = [&](hpar_status s) {
+    delete n;
+    return s;
+  };
+  if (cfg->nccl_comm) {
+    hpar_status s = need_nccl();
+    if (s) return bail(s);
+    int cnt = 0, rk = 0;
+    ncclResult_t r = g_nccl.commCount((ncclComm_t)cfg->nccl_comm, &cnt);
+    if (r != ncclSuccess) return bail(nccl_fail(r, (ncclComm_t)cfg->nccl_comm, "ncclCommCount"));
+    r = g_nccl.commUserRank((ncclComm_t)cfg->nccl_comm, &rk);
+    if (r != ncclSuccess) return bail(nccl_fail(r, (ncclComm_t)cfg->nccl_comm, "ncclCommUserRank"));
+    n->nranks = cnt;
+    n->rank = rk;
+  }
+  if (n->rank < 0 || n->rank >= n->nranks)
+    return bail(fail(HPAR_E_INVALID, "rank %d out of range for %d ranks", n->rank, n->nranks));
+
+  // ---- structural validation (contiguity, ranges, loops, schedules) ----
+  for (int a = 0; a < nlevels; ++a) {
+    const hpar_nest_level& L = lv[a];
+    n->user[a] = L;
+    if (L.first < HPAR_GPU || L.last > HPAR_LANE || L.first > L.last)
+      return bail(fail(HPAR_E_INVALID, "nest level %d: hardware range [%d,%d] outside gpu..lane", a, L.first, L.last));
+    if (L.loop != 0 && L.loop != 1) return bail(fail(HPAR_E_INVALID, "nest level %d: loop must be 0 or 1", a));
+    if (L.schedule < 0 || L.schedule > 3) return bail(fail(HPAR_E_INVALID, "nest level %d: bad schedule", a));
+    if ((L.schedule == HPAR_SCHED_STATIC_CHUNK || L.schedule == HPAR_SCHED_DYNAMIC) && L.chunk < 1)
+      return bail(fail(HPAR_E_INVALID, "nest level %d: %s needs chunk >= 1", a, sched_name(L.schedule)));
+    if (L.width < 0) return bail(fail(HPAR_E_PARTITION, "nest level %d: partition width %d < 1", a, L.width));
+    if (L.width > 0 && L.last != HPAR_LANE)
+      return bail(fail(HPAR_E_UNSUPPORTED, "nest level %d: only the lane level can be partitioned", a));
+    if (a > 0) {
+      const hpar_nest_level& P = lv[a - 1];
+      const int expect = P.width > 0 ? P.last : P.last + 1;
+      if (L.first != expect)
+        return bail(fail(HPAR_E_INVALID,
+                         "nest level %d: levels must be contiguous (collapse of a contiguous run, P:149-155): "
+                         "expected first=%d, got %d", a, expect, L.first));
+    }
+  }
+  if (lv[nlevels - 1].last != HPAR_LANE || lv[nlevels - 1].width != 0)
+    return bail(fail(HPAR_E_INVALID, "the innermost nest level must end at the lane level (unpartitioned)"));
+  if (n->nranks > 1 && lv[0].first != HPAR_GPU)
+    return bail(fail(HPAR_E_INVALID, "%d ranks: the outermost nest level must bind the GPU level", n->nranks));
+
+  // ---- geometry ----
+  int64_t K = cfg->cluster_dim > 0 ? cfg->cluster_dim : 2;
+  int64_t W = cfg->warps_per_cta > 0 ? cfg->warps_per_cta : 8;
+  int64_t C = cfg->clusters > 0 ? cfg->clusters : 0;
+  const int top = lv[0].first;
+  if (top > HPAR_GPU && n->nranks != 1) return bail(fail(HPAR_E_INVALID, "nest without GPU level needs 1 rank"));
+  if (top > HPAR_CLUSTER) {
+    if (C > 1) return bail(fail(HPAR_E_INVALID, "nest without cluster level: clusters must be 1"));
+    C = 1;
+  }
+  if (top > HPAR_CTA) K = 1;
+  if (top > HPAR_WARP) W = 1;
+  if (K < 1 || K > 16) return bail(fail(HPAR_E_INVALID, "cluster_dim %lld outside 1..16", (long long)K));
+  if (W < 1 || W > 32) return bail(fail(HPAR_E_INVALID, "warps_per_cta %lld outside 1..32", (long long)W));
+  int lane_w = 1;
+  for (int a = 0; a < nlevels; ++a) {
+    if (lv[a].width > 0) {
+      if (32 % lv[a].width != 0)
+        return bail(fail(HPAR_E_PARTITION, "nest level %d: width %d does not divide the lane level's num 32 (S:97)",
+                         a, lv[a].width));
+      lane_w = lv[a].width;
+      n->lane_part = true;
+    }
+  }
+  // fanouts fixing C
+  for (int a = 0; a < nlevels; ++a) {
+    const hpar_nest_level& L = lv[a];
+    if (L.fanout == 0) continue;
+    const bool inner_slice = a > 0 && lv[a - 1].width > 0;
+    int64_t prod = 1;
+    bool has_c = false;
+    for (int hw = L.first; hw <= L.last; ++hw) {
+      if (hw == HPAR_GPU) prod *= n->nranks;
+      else if (hw == HPAR_CLUSTER) has_c = true;
+      else if (hw == HPAR_CTA) prod *= K;
+      else if (hw == HPAR_WARP) prod *= W;
+      else if (hw == HPAR_LANE) {
+        if (L.width > 0) prod *= 32 / L.width;
+        else if (inner_slice) prod *= lane_w;
+        else prod *= 32;
+      }
+    }
+    if (has_c && C == 0) {
+      if (L.fanout % prod != 0)
+        return bail(fail(HPAR_E_INVALID, "nest level %d: fanout %lld not a multiple of %lld", a,
+                         (long long)L.fanout, (long long)prod));
+      C = L.fanout / prod;
+    } else {
+      if (has_c) prod *= C;
+      if (prod != L.fanout)
+        return bail(fail(HPAR_E_INVALID, "nest level %d: fanout %lld does not match the geometry (%lld)", a,
+                         (long long)L.fanout, (long long)prod));
+    }
+  }
+  if (C == 0) {
+    if (describe_only) {
+      C = default_resident_clusters(*cfg->desc, (int)K, (int)W);
+    } else {
+      cudaDeviceProp p;
+      cudaError_t e = cudaGetDeviceProperties(&p, cfg->device);
+      if (e != cudaSuccess) return bail(fail(HPAR_E_CUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e)));
+      C = std::max<int64_t>(1, (int64_t)p.multiProcessorCount * hpar::flat_resident_ctas_per_sm((int)W) / K);
+    }
+  }
+  n->G = n->nranks;
+  n->C = C;
+  n->K = K;
+  n->W = W;
+  n->lane_w = lane_w;
+  n->radix[S_GPU] = n->nranks;
+  n->radix[S_CLUSTER] = C;
+  n->radix[S_CTA] = K;
+  n->radix[S_WARP] = W;
+  n->radix[S_LANE] = 32 / lane_w;
+  n->radix[S_LANE_IN] = lane_w;
+  if (top > HPAR_GPU) n->radix[S_GPU] = 1;
+
+  // ---- resolve every nest level: slots, T, flags; capability checks ----
+  n->gpu_level = -1;
+  int64_t max_dyn_slots = 0;
+  for (int a = 0; a < nlevels; ++a) {
+    const hpar_nest_level& L = lv[a];
+    const bool inner_slice = a > 0 && lv[a - 1].width > 0;
+    DevLevel& D = n->lv[a];
+    memset(&D, 0, sizeof(D));
+    D.sched = L.schedule;
+    D.loop = L.loop;
+    D.chunk = L.chunk;
+    D.sfirst = slot_first(L.first, inner_slice);
+    D.slast = slot_last(L.last, L.width > 0);
+    int64_t T = 1;
+    for (int s = D.sfirst; s <= D.slast; ++s) T *= n->radix[s];
+    D.T = T;
+    uint32_t fl = 0xFFFFFFFFu;
+    for (int hw = L.first; hw <= L.last; ++hw) fl &= level_props(hw);  // collapse: intersection
+    n->props[a] = fl;
+    if (D.sfirst == S_GPU) {
+      n->gpu_level = a;
+      if (n->nranks > 1 && (L.schedule != HPAR_SCHED_STATIC || L.loop != 0))
+        return bail(fail(HPAR_E_UNSUPPORTED,
+                         "nest level %d binds the GPU level: only static (block) over loop 0 across GPUs "
+                         "(shards must be contiguous; P:72 no cross-GPU dynamic)", a));
+    }
+    if (L.schedule == HPAR_SCHED_DYNAMIC) {
+      if (!(fl & HPAR_P_DYNAMIC))
+        return bail(fail(HPAR_E_CAPABILITY,
+                         "nest level %d (%s..%s): dynamic schedule on a level without the `dynamic` property "
+                         "(S:338, Table 2)", a, kLevelNames[L.first], kLevelNames[L.last]));
+      int64_t slots = 1;
+      for (int s = S_CLUSTER; s < D.sfirst; ++s) slots *= n->radix[s];
+      max_dyn_slots = std::max(max_dyn_slots, slots);
+    }
+  }
+
+  // ---- workspace ----
+  n->dyn_slots = max_dyn_slots;
+  if (!describe_only) {
+    cudaError_t e = cudaSetDevice(cfg->device);
+    if (e == cudaSuccess) e = cudaMalloc(&n->grid_ticket, 64);
+    if (e == cudaSuccess) e = cudaMemset(n->grid_ticket, 0, 64);
+    n->cluster_partials_bytes = (size_t)C * 256 * 8;
+    if (e == cudaSuccess) e = cudaMalloc(&n->cluster_partials, n->cluster_partials_bytes);
+    if (e == cudaSuccess && max_dyn_slots > 0) {
+      e = cudaMalloc(&n->dyn_tickets, (size_t)max_dyn_slots * 8);
+      if (e == cudaSuccess) e = cudaMemset(n->dyn_tickets, 0, (size_t)max_dyn_slots * 8);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&n->error_flag, 64);
+    if (e == cudaSuccess) e = cudaMemset(n->error_flag, 0, 64);
+    if (e == cudaSuccess) e = cudaMalloc(&n->barrier_word, 64);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      hpar_nest_destroy(n);
+      return fail(e == cudaErrorMemoryAllocation ? HPAR_E_NOMEM : HPAR_E_CUDA, "workspace: %s",
+                  cudaGetErrorString(e));
+    }
+  }
+  *out = n;
+  return ok();
+}
+
+extern "C" hpar_status hpar_nest_destroy(hpar_nest_t n) {
+  if (!n) return ok();
+  if (n->device >= 0) {
+    cudaSetDevice(n->device);
+    cudaFree(n->grid_ticket);
+    cudaFree(n->cluster_partials);
+    cudaFree(n->dyn_tickets);
+    cudaFree(n->error_flag);
+    cudaFree(n->barrier_word);
+  }
+  delete n;
+  return ok();
+}
+
+extern "C" hpar_status hpar_nest_info(hpar_nest_t n, hpar_nest_info_t* out) {
+  if (!n || !out) return fail(HPAR_E_INVALID, "hpar_nest_info: NULL argument");
+  memset(out, 0, sizeof(*out));
+  out->G = n->G;
+  out->C = n->C;
+  out->K = n->K;
+  out->W = n->W;
+  out->rank = n->rank;
+  out->nlevels = n->nlev;
+  out->lane_width = n->lane_part ? n->lane_w : 0;
+  int64_t total = 1;
+  for (int a = 0; a < n->nlev; ++a) {
+    out->tasks[a] = n->lv[a].T;
+    total *= n->lv[a].T;
+    out->total[a] = total;
+    out->props[a] = n->props[a];
+  }
+  out->threads_per_gpu = n->C * n->K * n->W * 32;
+  return ok();
+}
+
+extern "C" const char* hpar_last_kernel(hpar_nest_t n) { return n ? n->last_kernel.c_str() : ""; }
+
+namespace {
+// rank g's contiguous range of the outermost loop under the GPU-holding
+// level's static block schedule (§8(a) A2).
+void shard_of(const hpar_nest* n, int64_t n0, int32_t rank, int64_t* begin, int64_t* count) {
+  if (n->gpu_level < 0 || n->nranks == 1) {
+    *begin = 0;
+    *count = n0;
+    return;
+  }
+  const DevLevel& D = n->lv[n->gpu_level];
+  const int64_t P = D.T / n->nranks;  // tasks of that level per GPU
+  const int64_t q = n0 / D.T, r = n0 % D.T;
+  auto start = [&](int64_t t) { return t * q + std::min(t, r); };
+  *begin = start((int64_t)rank * P);
+  *count = start((int64_t)(rank + 1) * P) - *begin;
+}
+}  // namespace
+
+extern "C" hpar_status hpar_shard_range(hpar_nest_t n, int64_t n0, int32_t rank, int64_t* begin, int64_t* count) {
+  if (!n || !begin || !count) return fail(HPAR_E_INVALID, "hpar_shard_range: NULL argument");
+  if (rank < 0 || rank >= n->nranks) return fail(HPAR_E_INVALID, "rank %d out of range", rank);
+  if (n0 < 0) return fail(HPAR_E_INVALID, "n0 < 0");
+  shard_of(n, n0, rank, begin, count);
+  return ok();
+}
+
+// ------------------------------------------------------------ planner ----
+namespace {
+// maximal list length reaching nest level `upto` of loop `loop` (task 0 owns
+// the most for every schedule; under a dynamic level a child sees <= chunk)
+int64_t max_parent_len(const hpar_nest* n, int loop, int upto, int64_t extent) {
+  int64_t len = extent;
+  for (int a = 0; a < upto; ++a) {
+    const DevLevel& D = n->lv[a];
+    if (D.loop != loop) continue;
+    if (D.sched == SCHED_STATIC) len = len / D.T + (len % D.T ? 1 : 0);
+    else if (D.sched == SCHED_NONE) len = std::min<int64_t>(len, 1);
+    else if (D.sched == SCHED_DYNAMIC) len = std::min(len, D.chunk);
+    else {
+      const int64_t nch = (len + D.chunk - 1) / D.chunk;
+      const int64_t mine = nch > 0 ? (nch - 1) / D.T + 1 : 0;
+      len = std::min(len, mine * D.chunk);
+    }
+  }
+  return len;
+}
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case HPAR_I32: case HPAR_F32: return 4;
+    case HPAR_I64: case HPAR_F64: case HPAR_U64: return 8;
+    case HPAR_U8: return 1;
+  }
+  return 0;
+}
+}  // namespace
+
+extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce_desc* d, void* stream_) {
+  if (!n || !d) return fail(HPAR_E_INVALID, "hpar_parallel_for_reduce: NULL argument");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  // ---- op / dtype ----
+  const bool hist = d->op == HPAR_OP_HIST256;
+  if (d->op < 0 || d->op > 3) return fail(HPAR_E_UNSUPPORTED, "unknown op %d", d->op);
+  if (hist && d->in_dtype != HPAR_U8) return fail(HPAR_E_UNSUPPORTED, "hist256 needs uint8 input");
+  if (!hist && !(d->in_dtype == HPAR_I32 || d->in_dtype == HPAR_I64 || d->in_dtype == HPAR_F32 ||
+                 d->in_dtype == HPAR_F64))
+    return fail(HPAR_E_UNSUPPORTED, "op %d: input dtype %d not supported (i32/i64/f32/f64)", d->op, d->in_dtype);
+  if (d->nloops != 1 && d->nloops != 2) return fail(HPAR_E_INVALID, "nloops must be 1 or 2");
+  if (d->n0 < 0 || d->n1 < 0) return fail(HPAR_E_INVALID, "negative loop extent");
+  if (!d->out) return fail(HPAR_E_INVALID, "out is NULL");
+  for (int a = 0; a < n->nlev; ++a)
+    if (n->lv[a].loop >= d->nloops)
+      return fail(HPAR_E_INVALID, "nest level %d binds loop %d but the call has %d loop(s)", a, n->lv[a].loop,
+                  d->nloops);
+  const bool csr = d->nloops == 2 && d->offsets != nullptr;
+  if (d->nloops == 2 && !csr && d->ld < d->n1) return fail(HPAR_E_INVALID, "ld < n1");
+  if (d->keyed && d->nloops != 2) return fail(HPAR_E_INVALID, "keyed results need two loops");
+  if (hist && d->keyed) return fail(HPAR_E_UNSUPPORTED, "keyed histograms");
+
+  int64_t begin = 0, local = 0;
+  shard_of(n, d->n0, n->rank, &begin, &local);
+  if (local > 0 && !d->in) return fail(HPAR_E_INVALID, "in is NULL");
+
+  // ---- schedule(none) overflow (diagnose, never UB) ----
+  for (int a = 0; a < n->nlev; ++a) {
+    if (n->lv[a].sched != SCHED_NONE) continue;
+    const int loop = n->lv[a].loop;
+    int64_t extent = loop == 0 ? d->n0 : d->n1;
+    if (loop == 1 && csr) {
+      if (d->max_inner <= 0)
+        return fail(HPAR_E_INVALID, "nest level %d: schedule(none) over CSR rows needs desc->max_inner", a);
+      extent = d->max_inner;
+    }
+    if (d->nloops == 1 && loop == 0) extent = d->n0;
+    const int64_t len = max_parent_len(n, loop, a, extent);
+    if (len > n->lv[a].T)
+      return fail(HPAR_E_SCHEDULE,
+                  "nest level %d: schedule(none) with %lld iterations for %lld tasks (P:251 'more logical "
+                  "iterations than tasks')", a, (long long)len, (long long)n->lv[a].T);
+  }
+
+  // ---- build the kernel arguments ----
+  NestArgs A;
+  memset(&A, 0, sizeof(A));
+  A.nlev = n->nlev;
+  A.rank = n->rank;
+  for (int s = 0; s < S_NSLOTS; ++s) A.radix[s] = n->radix[s];
+  A.lane_w = n->lane_w;
+  A.K = (int32_t)n->K;
+  A.C = n->C;
+  A.threads_per_gpu = n->C * n->K * n->W * 32;
+  for (int a = 0; a < n->nlev; ++a) A.lv[a] = n->lv[a];
+  A.op = d->op;
+  A.in_dtype = d->in_dtype;
+  A.nloops = d->nloops;
+  A.keyed = d->keyed;
+  A.verify = d->verify;
+  A.in = d->in;
+  A.n1 = d->n1;
+  A.ld = d->ld ? d->ld : d->n1;
+  A.offsets = d->offsets;
+  A.out = d->out;
+  for (int a = 0; a < HPAR_MAX_NEST; ++a) A.partials[a] = d->level_partials[a];
+  A.owner = d->coverage_owner;
+  A.count = d->coverage_count;
+  A.fp = (unsigned long long*)d->fingerprint;
+  A.global_begin = d->global_begin;
+  A.grid_ticket = n->grid_ticket;
+  A.cluster_partials = n->cluster_partials;
+  A.error_flag = n->error_flag;
+  A.dyn_tickets = n->dyn_tickets;
+  A.dyn_slots = n->dyn_slots;
+  A.dyn_level = -1;
+
+  if ((d->verify & HPAR_VERIFY_COVERAGE) && (!d->coverage_owner || !d->coverage_count))
+    return fail(HPAR_E_INVALID, "verify coverage needs coverage_owner and coverage_count");
+  if ((d->verify & HPAR_VERIFY_FINGERPRINT) && !d->fingerprint)
+    return fail(HPAR_E_INVALID, "verify fingerprint needs fingerprint[3]");
+
+  // The device enumerates GLOBAL loop-0 positions with the full task ids
+  // (GPU digit = rank); `in` / offsets / out are the rank's shard, so the
+  // GPU-holding level is applied here: it is replaced by the rank's own list
+  // [0, local) (static block => contiguous shard, §8(a) A2).
+  A.n0 = local;
+  if (n->gpu_level >= 0 && n->nranks > 1) {
+    // the GPU-holding level keeps its sub-GPU digits: re-express it as a
+    // static level over the tasks of this GPU only
+    DevLevel& D = A.lv[n->gpu_level];
+    D.sfirst = S_CLUSTER <= D.slast ? S_CLUSTER : S_GPU;
+    if (D.slast == S_GPU) {
+      D.T = 1;
+    } else {
+      D.T = D.T / n->nranks;
+    }
+    A.radix[S_GPU] = 1;
+  }
+  if (n->gpu_level >= 0 && A.lv[n->gpu_level].slast == S_GPU) A.lv[n->gpu_level].host_applied = 1;
+
+  // keyed: loop-0 levels must be a prefix; the row owner is the last of them
+  if (d->keyed) {
+    int k = 0;
+    while (k < n->nlev && n->lv[k].loop == 0) ++k;
+    for (int a = k; a < n->nlev; ++a)
+      if (n->lv[a].loop != 1)
+        return fail(HPAR_E_INVALID, "keyed results: the levels bound to loop 0 must be the outermost ones");
+    if (k == 0) return fail(HPAR_E_UNSUPPORTED, "keyed results need loop 0 bound to an outer level");
+    A.first_inner = k;
+    A.owner_slot = n->lv[k - 1].slast;
+    if (A.owner_slot == S_GPU && k < n->nlev)
+      return fail(HPAR_E_CAPABILITY,
+                  "keyed results owned by the GPU level would combine across clusters, which have no "
+                  "barrier (P:178); bind loop 0 down to the cluster level or below");
+    const bool fin = d->in_dtype == HPAR_F32 || d->in_dtype == HPAR_F64;
+    if (fin && d->out_dtype != HPAR_F32 && d->out_dtype != HPAR_F64)
+      return fail(HPAR_E_INVALID, "keyed fp results: out_dtype must be f32 or f64");
+    if (!fin && d->out_dtype != HPAR_I64) return fail(HPAR_E_INVALID, "keyed int results: out_dtype must be i64");
+    A.out_dtype = d->out_dtype;
+  } else {
+    A.out_dtype = (d->in_dtype == HPAR_F32 || d->in_dtype == HPAR_F64) ? HPAR_F64 : HPAR_I64;
+  }
+
+  // ---- kernel choice: fused specialisation if the nest matches its shape ----
+  const char* why = nullptr;
+  const char* name = "generic";
+  cudaError_t e = cudaSuccess;
+  if (n->device < 0) return fail(HPAR_E_INVALID, "describe-only nest: validated, cannot execute");
+  CUDA_TRY(cudaSetDevice(n->device));
+  if (hist) {
+    if (!hist_matches(A, &why))
+      return fail(HPAR_E_UNSUPPORTED, "hist256: nest shape not supported by the histogram kernel: %s", why);
+    e = launch_hist(A, (int)n->W, stream, &name);
+  } else if (flat_matches(A, &why)) {
+    e = launch_flat(A, (int)n->W, stream, &name);
+  } else if (rowwise_matches(A, &why)) {
+    e = launch_rowwise(A, (int)n->W, stream, &name);
+  } else {
+    // generic interpreter: at most one dynamic level, on loop 0
+    int ndyn = 0;
+    for (int a = 0; a < n->nlev; ++a) {
+      if (n->lv[a].sched != SCHED_DYNAMIC) continue;
+      ++ndyn;
+      if (n->lv[a].loop != 0 && d->nloops == 2)
+        return fail(HPAR_E_UNSUPPORTED, "nest level %d: dynamic schedule on the inner loop (generic kernel)", a);
+      A.dyn_level = a;
+    }
+    if (ndyn > 1) return fail(HPAR_E_UNSUPPORTED, "generic kernel: at most one dynamic level");
+    if (A.dyn_level >= 0) {
+      for (int a = 0; a < A.dyn_level; ++a)
+        if (n->lv[a].loop == 0 && n->lv[a].sched == SCHED_DYNAMIC)
+          return fail(HPAR_E_UNSUPPORTED, "generic kernel: nested dynamic levels");
+    }
+    e = launch_generic(A, (int)(n->W * 32), stream);
+  }
+  if (e != cudaSuccess) return fail(HPAR_E_CUDA, "launch %s: %s", name, cudaGetErrorString(e));
+  n->last_kernel = name;
+
+  // ---- node level: one allreduce over NVLink (§8(a) A9) ----
+  if (!d->keyed && n->nranks > 1) {
+    hpar_status s = need_nccl();
+    if (s) return s;
+    ncclDataType_t t;
+    ncclRedOp_t op = d->op == HPAR_OP_MIN ? ncclMin : d->op == HPAR_OP_MAX ? ncclMax : ncclSum;
+    size_t cnt = 1;
+    if (hist) {
+      t = ncclUint64;
+      cnt = 256;
+    } else {
+      t = (d->in_dtype == HPAR_F32 || d->in_dtype == HPAR_F64) ? ncclFloat64 : ncclInt64;
+    }
+    ncclResult_t r = g_nccl.allReduce(d->out, d->out, cnt, t, op, (ncclComm_t)n->comm, stream);
+    if (r != ncclSuccess) return nccl_fail(r, (ncclComm_t)n->comm, "ncclAllReduce");
+  }
+  (void)dtype_size;
+  return ok();
+}
+
+// ----------------------------------------------------------- barriers ----
+extern "C" hpar_status hpar_barrier(hpar_nest_t n, int32_t level, uint64_t* mismatches, void* stream_) {
+  if (!n) return fail(HPAR_E_INVALID, "hpar_barrier: NULL nest");
+  if (level < HPAR_NODE || level > HPAR_LANE) return fail(HPAR_E_INVALID, "bad level %d", level);
+  if (!(level_props(level) & HPAR_P_BARRIER) && level != HPAR_NODE)
+    return fail(HPAR_E_CAPABILITY, "barrier on the %s level, which has no `barrier` property (S:348; P:178)",
+                kLevelNames[level]);
+  if (n->device < 0) return fail(HPAR_E_INVALID, "describe-only nest cannot execute");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (level == HPAR_NODE) return ok();
+  CUDA_TRY(cudaSetDevice(n->device));
+  if (level == HPAR_GPU) {
+    if (n->nranks == 1 || !n->comm) return ok();
+    hpar_status s = need_nccl();
+    if (s) return s;
+    ncclResult_t r = g_nccl.allReduce(n->barrier_word, n->barrier_word, 1, ncclInt32, ncclSum, (ncclComm_t)n->comm,
+                                      stream);
+    if (r != ncclSuccess) return nccl_fail(r, (ncclComm_t)n->comm, "ncclAllReduce (barrier)");
+    return ok();
+  }
+  cudaError_t e = launch_probe(level, n->C, (int)n->K, (int)n->W, 8, (unsigned long long*)mismatches, stream);
+  if (e != cudaSuccess) return fail(HPAR_E_CUDA, "barrier probe: %s", cudaGetErrorString(e));
+  return ok();
+}

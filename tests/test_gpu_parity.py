@@ -1,0 +1,349 @@
+"""GPU parity: libhpar.so (through the C ABI) against the oracle, element by
+element, on seeded inputs.  Bit-exact for integers, coverage maps and bins;
+1e-5 relative for fp32 (north_star).  Runs on the B200 box (-m gpu)."""
+import random
+
+import numpy as np
+import pytest
+
+from inputs import gen
+from tests.nestutil import assert_rel, fanouts, oracle_levels
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2309_01906_b200 import build
+    build.build()
+    from paper_2309_01906_b200 import hpar
+    return hpar
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    import torch
+    return torch
+
+
+@pytest.fixture(scope="module")
+def inputs_lib():
+    import ctypes
+    import os
+    from paper_2309_01906_b200 import build
+    build.build()
+    L = ctypes.CDLL(os.path.join(os.path.dirname(gen.__file__), "libhpar_inputs.so"))
+    for name in ("hpar_inputs_fill_i32", "hpar_inputs_fill_f32", "hpar_inputs_fill_u8"):
+        f = getattr(L, name)
+        f.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        f.restype = ctypes.c_int
+    return L
+
+
+def dev_fill(L, torch, kind, seed, begin, n):
+    dt = {"i32": torch.int32, "f32": torch.float32, "u8": torch.uint8}[kind]
+    t = torch.empty(n, dtype=dt, device="cuda")
+    rc = getattr(L, f"hpar_inputs_fill_{kind}")(seed, begin, n, t.data_ptr(), None)
+    assert rc == 0
+    return t
+
+
+def test_device_generator_matches_numpy(inputs_lib, torch_mod):
+    torch = torch_mod
+    for kind, f in (("i32", gen.gen_i32), ("f32", gen.gen_f32), ("u8", gen.gen_u8)):
+        for seed, begin in ((1, 0), (5, (1 << 34) - 5000)):
+            t = dev_fill(inputs_lib, torch, kind, seed, begin, 5000)
+            assert np.array_equal(t.cpu().numpy(), f(seed, begin, 5000))
+
+
+# ---------------------------------------------------------------------------
+def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, C=4, K=2, W=4,
+             partials=True, coverage=True, max_inner=0, out_f64=True):
+    nest = H.Nest(levels, device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+    nloops = 2 if (n1 or offsets is not None) else 1
+    if offsets is not None:
+        n_iter = int(offsets[-1])
+    else:
+        n_iter = n0 * (n1 if nloops == 2 else 1)
+    xd = torch.from_numpy(x).cuda()
+    fp = x.dtype.kind == "f"
+    if keyed:
+        out = torch.zeros(n0, dtype=torch.float64 if fp else torch.int64, device="cuda")
+    elif op == H.OP_HIST256:
+        out = torch.zeros(256, dtype=torch.int64, device="cuda")
+    else:
+        out = torch.zeros(1, dtype=torch.float64 if fp else torch.int64, device="cuda")
+    owner = torch.full((max(n_iter, 1),), -1, dtype=torch.int64, device="cuda") if coverage else None
+    count = torch.zeros(max(n_iter, 1), dtype=torch.int32, device="cuda") if coverage else None
+    Ts = fanouts(levels, 1, C, K, W)
+    parts = []
+    if partials:
+        first_inner = 0
+        if keyed:
+            while first_inner < len(levels) and levels[first_inner].loop == 0:
+                first_inner += 1
+        tot = 1
+        for a, T in enumerate(Ts):
+            if keyed:
+                if a < first_inner:
+                    parts.append(None)
+                    continue
+                per = int(np.prod(Ts[first_inner:a + 1]))
+                size = n0 * per
+            else:
+                tot *= T
+                size = tot
+            shape = (size, 256) if op == H.OP_HIST256 else (size,)
+            parts.append(torch.full(shape, -7, dtype=torch.float64 if (fp and op != H.OP_HIST256) else torch.int64,
+                                    device="cuda"))
+    offs = torch.from_numpy(offsets).cuda() if offsets is not None else None
+    verify = (H.VERIFY_COVERAGE if coverage else 0) | (H.VERIFY_PARTIALS if partials else 0)
+    d = H.make_desc(xd, out, op=op, n0=n0, n1=n1, ld=n1, nloops=nloops, keyed=keyed, offsets=offs,
+                    max_inner=max_inner, verify=verify, partials=parts, owner=owner, count=count,
+                    out_dtype=(H.F64 if fp else H.I64) if keyed else -1)
+    nest.parallel_for_reduce(d)
+    torch.cuda.synchronize()
+    res = out.cpu().numpy()
+    return dict(nest=nest, out=res, owner=owner.cpu().numpy()[:n_iter] if coverage else None,
+                count=count.cpu().numpy()[:n_iter] if coverage else None,
+                parts=[p.cpu().numpy() if p is not None else None for p in parts], kernel=nest.last_kernel())
+
+
+def compare(oracle, H, levels, res, x, *, n0, n1=0, offsets=None, keyed=False, op=0, C, K, W,
+            dynamic=False, partials=True):
+    ol = oracle_levels(oracle, levels, 1, C, K, W)
+    o = oracle.nest_run(ol, n0=n0, n1=n1, offsets=offsets, x=x, op=op, keyed=keyed,
+                        nloops=2 if (n1 or offsets is not None) else 1)
+    fp = x.dtype.kind == "f"
+    # result
+    if op == H.OP_HIST256:
+        assert np.array_equal(res["out"].astype(np.uint64), o.result)
+    elif fp:
+        assert_rel(res["out"] if keyed else res["out"][0], o.result)
+    else:
+        assert np.array_equal(res["out"] if keyed else res["out"][0], o.result)
+    # coverage
+    if res["count"] is not None:
+        assert (res["count"] == 1).all(), "every iteration executes exactly once"
+        if not dynamic:
+            assert np.array_equal(res["owner"], o.owner), "owner map differs from the oracle"
+    # partials (static nests; dynamic assignment differs from the round-robin model)
+    if partials and not dynamic:
+        for a, p in enumerate(res["parts"]):
+            if p is None or o.partials[a] is None:
+                continue
+            if op == H.OP_HIST256:
+                if np.all(p == -7):
+                    continue  # level without materialised bins (lanes)
+                assert np.array_equal(p.astype(np.uint64), o.partials[a]), f"level {a} partials"
+            elif fp:
+                assert_rel(p, o.partials[a])
+            else:
+                assert np.array_equal(p, o.partials[a]), f"level {a} partials"
+    return o
+
+
+# ---------------------------------------------------------------------------
+def test_c1_generic_bit_exact(H, torch_mod, oracle):
+    """Config 1 at full size (2^20 int32, outer 1024 x inner 1024): int64 sum,
+    coverage owner map and per-level partials bit-exact."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    x = gen.gen_i32(gen.SEED_C1, 0, 1 << 20)
+    levels = nests.c1_nest(with_gpu=True)
+    C, K, W = 512, 2, 8
+    res = run_nest(H, torch, levels, x, n0=1024, n1=1024, C=C, K=K, W=W)
+    assert res["out"][0] == oracle.sum_i32(x)
+    compare(oracle, H, levels, res, x, n0=1024, n1=1024, C=C, K=K, W=W)
+
+
+SCHEDS = [(0, 0), (1, 1), (1, 3), (1, 8), (3, 0)]
+
+
+def random_flat_nest(H, rng, n):
+    """random nest over gpu..lane with collapses and an optional lane partition"""
+    hw = [H.HPAR_GPU, H.HPAR_CLUSTER, H.HPAR_CTA, H.HPAR_WARP, H.HPAR_LANE]
+    cuts = sorted(rng.sample(range(1, 5), rng.randint(1, 4)))
+    bounds = [0] + cuts + [5]
+    levels = []
+    for i in range(len(bounds) - 1):
+        s, c = rng.choice(SCHEDS)
+        levels.append(H.Level(hw[bounds[i]], hw[bounds[i + 1] - 1], s, loop=0, chunk=c))
+    if rng.random() < 0.4:
+        w = rng.choice([2, 4, 8, 16])
+        levels[-1].width = w
+        levels.append(H.Level(H.HPAR_LANE, H.HPAR_LANE, rng.choice([0, 1]), loop=0, chunk=rng.choice([1, 2])))
+    return levels
+
+
+def test_generic_random_flat_nests(H, torch_mod, oracle):
+    """≥40 random flat nests (collapses, partitions, every static schedule,
+    ragged sizes): results, owner maps and partials vs the oracle."""
+    torch = torch_mod
+    rng = random.Random(2309)
+    done = 0
+    while done < 40:
+        levels = random_flat_nest(H, rng, 0)
+        C, K, W = rng.choice([1, 3, 5]), rng.choice([1, 2, 4]), rng.choice([1, 2, 4])
+        n = rng.randint(0, 7000)
+        Ts = fanouts(levels, 1, C, K, W)
+        # skip nests whose schedule(none) would overflow (tested separately)
+        try:
+            oracle.nest_run(oracle_levels(oracle, levels, 1, C, K, W), n0=n)
+        except oracle.OracleError:
+            with pytest.raises(H.HparError) as e:
+                run_nest(H, torch, levels, gen.gen_i32(7, 0, max(n, 1))[:n], n0=n, C=C, K=K, W=W)
+            assert e.value.code == H.HPAR_E_SCHEDULE
+            continue
+        x = gen.gen_i32(done + 100, 0, n) if done % 2 == 0 else gen.gen_f32(done + 100, 0, n)
+        res = run_nest(H, torch, levels, x, n0=n, C=C, K=K, W=W)
+        compare(oracle, H, levels, res, x, n0=n, C=C, K=K, W=W)
+        done += 1
+        assert Ts
+
+
+def test_generic_min_max(H, torch_mod, oracle):
+    torch = torch_mod
+    levels = [H.Level(H.HPAR_CLUSTER, H.HPAR_CTA, 1, chunk=5), H.Level(H.HPAR_WARP, H.HPAR_LANE, 0)]
+    for x in (gen.gen_f32(3, 0, 9999), gen.gen_i32(3, 0, 9999)):
+        for op in (H.OP_MIN, H.OP_MAX):
+            res = run_nest(H, torch, levels, x, n0=x.size, op=op, C=3, K=2, W=2)
+            compare(oracle, H, levels, res, x, n0=x.size, op=op, C=3, K=2, W=2)
+
+
+def test_generic_two_loop_total_and_keyed(H, torch_mod, oracle):
+    """Multi-loop nests (P:215-225 bind_ancestor): dense and CSR, total and
+    keyed, including a lane partition for the keyed CSR rows."""
+    torch = torch_mod
+    rng = random.Random(5)
+    # dense keyed: rows over cluster(s) or CTAs, cols over the rest
+    for rows_to in (H.HPAR_CLUSTER, H.HPAR_CTA, H.HPAR_WARP):
+        levels = [H.Level(H.HPAR_GPU, H.HPAR_GPU, 0, loop=0),
+                  H.Level(H.HPAR_CLUSTER, rows_to, rng.choice([0, 1]), loop=0, chunk=2)]
+        if rows_to < H.HPAR_LANE:
+            levels.append(H.Level(rows_to + 1, H.HPAR_LANE, rng.choice([0, 1]), loop=1, chunk=rng.choice([1, 4])))
+        n0, n1 = 37, 301
+        x = gen.gen_f32(11, 0, n0 * n1)
+        res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=True, C=3, K=2, W=4)
+        compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, C=3, K=2, W=4)
+        xi = gen.gen_i32(12, 0, n0 * n1)
+        res = run_nest(H, torch, levels, xi, n0=n0, n1=n1, keyed=False, C=3, K=2, W=4)
+        compare(oracle, H, levels, res, xi, n0=n0, n1=n1, keyed=False, C=3, K=2, W=4)
+    # CSR keyed with lanes(8) groups owning rows
+    off = gen.csr_offsets(500, 9000)
+    v = gen.gen_f32(gen.SEED_C3, 0, 9000)
+    levels = [H.Level(H.HPAR_GPU, H.HPAR_GPU, 0, loop=0), H.Level(H.HPAR_CLUSTER, H.HPAR_CTA, 0, loop=0),
+              H.Level(H.HPAR_WARP, H.HPAR_LANE, 1, loop=0, chunk=1, width=8),
+              H.Level(H.HPAR_LANE, H.HPAR_LANE, 1, loop=1, chunk=1)]
+    res = run_nest(H, torch, levels, v, n0=500, offsets=off, keyed=True, C=2, K=2, W=2)
+    compare(oracle, H, levels, res, v, n0=500, offsets=off, keyed=True, C=2, K=2, W=2)
+
+
+def test_generic_dynamic_levels(H, torch_mod, oracle):
+    """dynamic(c) at the cluster, CTA and warp levels: every iteration once,
+    each task's iterations a union of whole chunks of its parent list, results
+    equal (reading #9)."""
+    torch = torch_mod
+    for dyn_first, dyn_last in ((H.HPAR_CLUSTER, H.HPAR_CLUSTER), (H.HPAR_CLUSTER, H.HPAR_CTA),
+                                (H.HPAR_WARP, H.HPAR_WARP)):
+        levels = []
+        hw = H.HPAR_CLUSTER
+        if dyn_first > hw:
+            levels.append(H.Level(hw, dyn_first - 1, 0))
+        levels.append(H.Level(dyn_first, dyn_last, H.DYNAMIC, chunk=37))
+        if dyn_last < H.HPAR_LANE:
+            levels.append(H.Level(dyn_last + 1, H.HPAR_LANE, 1, chunk=1))
+        x = gen.gen_i32(21, 0, 50000)
+        res = run_nest(H, torch, levels, x, n0=x.size, C=5, K=2, W=4)
+        compare(oracle, H, levels, res, x, n0=x.size, C=5, K=2, W=4, dynamic=True)
+        if (dyn_first, dyn_last) == (H.HPAR_CLUSTER, H.HPAR_CLUSTER):
+            # chunk alignment: every chunk of 37 consecutive iterations belongs to one cluster
+            cl = res["owner"] // (2 * 4 * 32)
+            pad = (-x.size) % 37
+            chunks = np.concatenate([cl, np.full(pad, -1)]).reshape(-1, 37)
+            for row in chunks:
+                vals = row[row >= 0]
+                assert (vals == vals[0]).all()
+    # keyed CSR with dynamic rows over teams (config-3 generic nest)
+    from paper_2309_01906_b200 import nests
+    off = gen.csr_offsets(3000, 40000)
+    v = gen.gen_f32(gen.SEED_C3, 0, 40000)
+    levels = nests.c3_nest(with_gpu=True, rows_chunk=16, width=8)
+    res = run_nest(H, torch, levels, v, n0=3000, offsets=off, keyed=True, C=4, K=2, W=4)
+    compare(oracle, H, levels, res, v, n0=3000, offsets=off, keyed=True, C=4, K=2, W=4, dynamic=True)
+
+
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [0, 1, 5, 4096 * 2 * 7 + 3, 1 << 20, (1 << 22) + 4 * 12345 + 2])
+def test_flat_fused_kernel(H, torch_mod, oracle, n):
+    """The fused TMA flat kernel (config-5 nest) at reduced sizes with ragged
+    tails: sum bit-comparable within 1e-5, owner map and partials vs oracle."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c5_nest(K=2)
+    C, K, W = 7, 2, 8
+    x = gen.gen_f32(gen.SEED_C5, 0, n)
+    res = run_nest(H, torch, levels, x, n0=n, C=C, K=K, W=W, coverage=n <= (1 << 20))
+    assert res["kernel"] == "flat_tma"
+    compare(oracle, H, levels, res, x, n0=n, C=C, K=K, W=W, partials=n <= (1 << 20))
+    xi = gen.gen_i32(gen.SEED_C1, 0, n)
+    res = run_nest(H, torch, levels, xi, n0=n, C=C, K=K, W=W, coverage=False, partials=False)
+    assert res["out"][0] == oracle.sum_i32(xi)
+
+
+def test_rowwise_fused_kernel_small(H, torch_mod, oracle):
+    """The fused row-wise kernel (config-2 nest) on 50 x 4096 and ragged
+    columns: rows, owner map, per-row lane/warp/CTA partials vs oracle."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c2_nest()
+    for n0, n1, C in ((50, 4096, 7), (13, 1000, 3), (5, 8, 9)):
+        x = gen.gen_f32(gen.SEED_C2, 0, n0 * n1)
+        res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=True, C=C, K=2, W=8)
+        assert res["kernel"] == "rowwise_tma_dsmem"
+        compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, C=C, K=2, W=8)
+
+
+@pytest.mark.parametrize("n", [0, 17, 16384 * 2 * 5 + 7, 1 << 20])
+def test_hist_fused_kernel(H, torch_mod, oracle, n):
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c4_nest(K=2)
+    C, K, W = 5, 2, 8
+    for x in (gen.gen_u8(gen.SEED_C4, 0, n), gen.gen_u8_zipf(gen.SEED_C4, 0, n), np.zeros(n, np.uint8)):
+        res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, coverage=n <= 200000,
+                       partials=n <= 200000)
+        assert res["kernel"] == "hist256_tma"
+        assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
+        if n <= 200000:
+            compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
+
+
+def test_barrier_probes(H, torch_mod):
+    """§8(a) A10: lane / warp / CTA barriers give rendezvous + visibility
+    (0 mismatches); the cluster level has no barrier."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    nest = H.Nest(nests.c5_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=37)
+    mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for lvl in (H.HPAR_LANE, H.HPAR_WARP, H.HPAR_CTA, H.HPAR_NODE, H.HPAR_GPU):
+        nest.barrier(lvl, mm.data_ptr())
+    torch.cuda.synchronize()
+    assert int(mm.item()) == 0
+    with pytest.raises(H.HparError) as e:
+        nest.barrier(H.HPAR_CLUSTER, mm.data_ptr())
+    assert e.value.code == H.HPAR_E_CAPABILITY
+
+
+def test_hierarchy_query_matches_device(H, torch_mod):
+    torch = torch_mod
+    t = H.hpar_hierarchy_query(0)
+    p = torch.cuda.get_device_properties(0)
+    assert [r.name.decode() for r in t] == H.LEVEL_NAMES
+    assert t[H.HPAR_GPU].num == 1 and t[H.HPAR_LANE].num == 32
+    assert t[H.HPAR_GPU].groupmem_bytes == p.total_memory
+    assert t[H.HPAR_CLUSTER].num >= p.multi_processor_count // 2
+    assert "barrier" not in t[H.HPAR_CLUSTER].flags() and "shuffle" in t[H.HPAR_LANE].flags()
