@@ -1,0 +1,421 @@
+#!/usr/bin/env python3
+"""bench.py — throughput of the hpar hot path on B200 (BASELINE.json metric:
+"elements/s and HBM GB/s (% of peak) for nested reductions at 1/2/4/8 B200").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c5|c4|c1|c3] [--impl hpar|reference]
+
+A step is one hpar_parallel_for_reduce over one batch of the config's
+synthetic workload (seeded generator, inputs/gen.py recipe), inputs resident
+in HBM.  Default workload: config 2 (BASELINE.json configs[1]), the 4-level
+row-wise nest over a 65536 x 4096 fp32 matrix per GPU (weak scaling: each
+rank reduces its own 65536-row shard; rows are independent, no collective).
+Config 5 (2^34 fp32 flat sum over the GPUs, one NCCL allreduce) is
+strong-scaled.  Under torchrun one process per GPU; rank 0 prints ONE JSON
+line.  `--impl reference` times the CPU oracle (the reference arm for this
+tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "elements/s and HBM GB/s (% of peak) for nested reductions at 1/2/4/8 B200"
+NOMINAL_HBM_GBS = 8000.0
+L2_BYTES = 126 * 2 ** 20
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------- clocks --
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.marks = [None, None]
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def mark(self, i):
+        self.marks[i] = time.time()
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+        rows = []
+        t0, t1 = self.marks
+        for ts, line in self.samples:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            rows.append((ts, parts))
+        inside = [r for r in rows if t0 and t1 and t0 - 0.05 <= r[0] <= t1 + 0.05] or rows
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(p[0]) for _, p in inside if p[0].replace(".", "").isdigit()]
+        smax = [float(p[1]) for _, p in inside if p[1].replace(".", "").isdigit()]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[k] for _, p in inside for k in range(4) if p[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(inside)}
+
+
+# --------------------------------------------------------------- configs --
+def config_spec(name: str, nranks: int):
+    from inputs import gen
+    if name == "c2":
+        rows, cols = 65536, 4096
+        return dict(workload="c2_rowwise_4level_65536x4096_f32", kind="rowwise", rows_per_rank=rows, cols=cols,
+                    n0=rows * nranks, scaling="weak", seed=gen.SEED_C2, dtype="f32",
+                    elems_per_rank=rows * cols, bytes_per_rank=rows * cols * 4 + rows * 4)
+    if name == "c5":
+        n = 1 << 34
+        return dict(workload="c5_flat_5level_2^34_f32", kind="flat", n0=n, scaling="strong", seed=gen.SEED_C5,
+                    dtype="f32", elems_total=n)
+    if name == "c4":
+        n = 1 << 32
+        return dict(workload="c4_hist256_2^32_u8", kind="hist", n0=n, scaling="strong", seed=gen.SEED_C4,
+                    dtype="u8", elems_total=n)
+    if name == "c1":
+        return dict(workload="c1_2level_1024x1024_i32", kind="c1", n0=1024, cols=1024, scaling="weak",
+                    seed=gen.SEED_C1, dtype="i32", elems_per_rank=1 << 20, bytes_per_rank=(1 << 22) + 8)
+    if name == "c3":
+        return dict(workload="c3_csr_segmented_2^24rows_2^28nnz_f32", kind="csr", rows=1 << 24, nnz=1 << 28,
+                    scaling="weak", seed=gen.SEED_C3, dtype="f32", elems_per_rank=1 << 28,
+                    bytes_per_rank=(1 << 30) + ((1 << 24) + 1) * 8 + (1 << 24) * 4)
+    raise SystemExit(f"unknown config {name}")
+
+
+# ------------------------------------------------------------- hpar arm ---
+def run_hpar(args):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_01906_b200 import build as pbuild
+    if int(os.environ.get("RANK", "0")) == 0:
+        pbuild.build()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+        pbuild.build()  # no-op after rank 0 built
+    from paper_2309_01906_b200 import hpar as H
+    from paper_2309_01906_b200 import nests
+
+    comm = None
+    if world > 1:
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)
+        comm = H.torch_nccl_comm()
+    spec = config_spec(args.config, world)
+    L = ctypes.CDLL(os.path.join(ROOT, "inputs", "libhpar_inputs.so"))
+    for f in ("hpar_inputs_fill_f32", "hpar_inputs_fill_u8", "hpar_inputs_fill_i32"):
+        getattr(L, f).argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    # tuned geometry per config (sweeps in profiles/)
+    tuned = {"c2": (4, 888)}.get(args.config, (8, 0))
+    K = 2
+    W = args.warps or tuned[0]
+    if args.clusters < 0:
+        args.clusters = tuned[1]
+    kind = spec["kind"]
+    if kind == "rowwise":
+        nest = H.Nest(nests.c2_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+                      clusters=args.clusters)
+        b, cnt = nest.shard_range(spec["n0"], rank)
+        cols = spec["cols"]
+        x = torch.empty(cnt * cols, dtype=torch.float32, device=dev)
+        L.hpar_inputs_fill_f32(spec["seed"], b * cols, cnt * cols, x.data_ptr(), sptr)
+        out = torch.empty(cnt, dtype=torch.float32, device=dev)
+        desc = H.make_desc(x, out, n0=spec["n0"], n1=cols, ld=cols, nloops=2, keyed=True)
+        elems_rank = cnt * cols
+        alg_bytes = cnt * cols * 4 + cnt * 4
+        host_in_bytes, host_out_bytes = cnt * cols * 4, cnt * 4
+    elif kind in ("flat", "hist"):
+        if kind == "flat":
+            nest = H.Nest(nests.c5_nest(K), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+                          clusters=args.clusters)
+        else:
+            nest = H.Nest(nests.c4_nest(K), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+                          clusters=args.clusters)
+        b, cnt = nest.shard_range(spec["n0"], rank)
+        if kind == "flat":
+            x = torch.empty(cnt, dtype=torch.float32, device=dev)
+            L.hpar_inputs_fill_f32(spec["seed"], b, cnt, x.data_ptr(), sptr)
+            out = torch.empty(1, dtype=torch.float64, device=dev)
+            alg_bytes = cnt * 4 + 8
+            host_in_bytes = cnt * 4
+        else:
+            x = torch.empty(cnt, dtype=torch.uint8, device=dev)
+            L.hpar_inputs_fill_u8(spec["seed"], b, cnt, x.data_ptr(), sptr)
+            out = torch.empty(256, dtype=torch.int64, device=dev)
+            alg_bytes = cnt + 2048
+            host_in_bytes = cnt
+        desc = H.make_desc(x, out, n0=spec["n0"], op=H.OP_HIST256 if kind == "hist" else H.OP_SUM)
+        elems_rank = cnt
+        host_out_bytes = out.numel() * out.element_size()
+    elif kind == "c1":
+        nest = H.Nest(nests.c1_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W)
+        b, cnt = nest.shard_range(spec["n0"] * world, rank)
+        x = torch.empty(cnt * 1024, dtype=torch.int32, device=dev)
+        L.hpar_inputs_fill_i32(spec["seed"], b * 1024, cnt * 1024, x.data_ptr(), sptr)
+        out = torch.empty(1, dtype=torch.int64, device=dev)
+        desc = H.make_desc(x, out, n0=spec["n0"] * world, n1=1024, ld=1024, nloops=2)
+        elems_rank = cnt * 1024
+        alg_bytes = cnt * 1024 * 4 + 8
+        host_in_bytes, host_out_bytes = cnt * 4096, 8
+    else:
+        raise SystemExit("config c3 is not wired into bench.py yet")
+    torch.cuda.synchronize()
+
+    def step():
+        nest.parallel_for_reduce(desc, sptr)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # L2: inputs are larger than L2 for c2/c4/c5 (no flush needed); for c1 flush
+    flush = None
+    if alg_bytes < 3 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.mark(0)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_all0 = torch.cuda.Event(enable_timing=True)
+    t_all1 = torch.cuda.Event(enable_timing=True)
+    t_all0.record(stream)
+    for i in range(args.steps):
+        if flush is not None:
+            flush.fill_(1.0)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    t_all1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks.mark(1)
+    time.sleep(0.1)
+    clk = clocks.stop()
+    kern_ms = [a.elapsed_time(b_) for a, b_ in ev]
+    step_ms_local = sum(kern_ms) / len(kern_ms)
+    # max over ranks
+    t = torch.tensor([step_ms_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms = float(t.item())
+    elems_total = elems_rank * world if spec["scaling"] == "weak" else spec["n0"] * (1024 if kind == "c1" else 1)
+    if spec["scaling"] == "strong":
+        elems_total = spec["n0"]
+    value = elems_total / (step_ms * 1e-3)
+    peak, peak_src = measured_peak()
+    achieved = alg_bytes / (step_ms_local * 1e-3) / 1e9
+
+    # ---------------- e2e: host buffers through the C ABI ----------------
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        host_x = torch.empty(x.numel(), dtype=x.dtype, pin_memory=True)
+        host_x.copy_(x)
+        host_out = torch.empty(out.numel(), dtype=out.dtype, pin_memory=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            x.copy_(host_x, non_blocking=True)
+            step()
+            host_out.copy_(out, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": elems_total / (float(e2e_ms.item()) * 1e-3), "unit": "elements/s",
+               "h2d_bytes_per_step": int(host_in_bytes), "d2h_bytes_per_step": int(host_out_bytes),
+               "steps": e2e_steps, "ms_per_step": float(e2e_ms.item())}
+
+    kernel = nest.last_kernel()
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tj.get(f"{args.config}:{kernel}")
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": spec["scaling"],
+        "vs_baseline": None, "dtype": spec["dtype"], "data": "synthetic (seeded splitmix64, inputs/gen.py recipe)",
+        "config": {"workload": spec["workload"], "kernel": kernel, "n0_global": spec["n0"],
+                   "elements_total": elems_total, "parallelism": f"gpu{world}",
+                   "l2": "inputs > L2, no flush" if flush is None else "L2 flushed (256 MB write) before each step",
+                   "geometry": {"C": nest.info().C, "K": K, "W": W}},
+        "hbm_gbs": achieved * (world if spec["scaling"] == "weak" else 1) if False else achieved,
+        "pct_of_8tbs": achieved / NOMINAL_HBM_GBS,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "kernel": kernel,
+                     "algorithmic_bytes_per_launch": int(alg_bytes)},
+        "clocks": clk, "e2e": e2e, "gpu_launches": args.steps,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------ CPU oracle legs ---
+def cpu_baseline(config: str, budget_s: float = 10.0, samples: int = 1):
+    """Time the oracle (plain sequential C, one core) on a bounded sample of
+    the workload; returns elements/s and what was sampled."""
+    import numpy as np
+
+    from inputs import gen
+    from oracle import oracle as O
+    O.build()
+    cores = 1
+    if config == "c2":
+        cols = 4096
+        rows = 8192
+        a = gen.gen_f32(gen.SEED_C2, 0, rows * cols)
+        O.rowsum_f32(a[: 64 * cols], 64, cols)  # warm
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            O.rowsum_f32(a, rows, cols)
+            reps += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return {"value": reps * rows * cols / dt, "unit": "elements/s", "cores": cores, "kind": "oracle",
+                "sample": f"or_rowsum_f32 over {rows} rows x {cols} of the c2 matrix, {reps} passes, {dt:.1f} s"}
+    if config in ("c5", "c1"):
+        n = 1 << 26
+        x = gen.gen_f32(gen.SEED_C5, 0, n) if config == "c5" else gen.gen_i32(gen.SEED_C1, 0, n)
+        f = O.sum_f32 if config == "c5" else O.sum_i32
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            f(x)
+            reps += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return {"value": reps * n / dt, "unit": "elements/s", "cores": cores, "kind": "oracle",
+                "sample": f"{f.__name__} over the first 2^26 elements, {reps} passes, {dt:.1f} s"}
+    if config == "c4":
+        n = 1 << 26
+        x = gen.gen_u8(gen.SEED_C4, 0, n)
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            O.hist256(x)
+            reps += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return {"value": reps * n / dt, "unit": "elements/s", "cores": cores, "kind": "oracle",
+                "sample": f"or_hist256 over the first 2^26 bytes, {reps} passes, {dt:.1f} s"}
+    return None
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # one step = the oracle over a bounded sample of the workload, sized so the
+    # whole --warmup + --steps run ends within ~2 minutes
+    total_budget = 120.0
+    per_step = max(0.01, total_budget / max(1, args.steps + args.warmup))
+    base = cpu_baseline(args.config, budget_s=min(per_step, 10.0))
+    spec = config_spec(args.config, 1)
+    value = base["value"]
+    elems_step = value * per_step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": elems_step / value * 1e3,
+        "higher_is_better": True, "scaling": spec["scaling"], "vs_baseline": None, "dtype": spec["dtype"],
+        "data": "synthetic (seeded splitmix64, inputs/gen.py recipe)",
+        "config": {"workload": spec["workload"], "kernel": "oracle (CPU, sequential C)"},
+        "cpu_baseline": base,
+        "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="hpar", choices=["hpar", "reference"])
+    ap.add_argument("--clusters", type=int, default=-1, help="C (0 = resident clusters, -1 = tuned default)")
+    ap.add_argument("--warps", type=int, default=0, help="W warps per CTA (0 = tuned default)")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_hpar(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
       if (lane == 0) mbar_arrive(&empty[s]);
     }
   }
+  __syncwarp();
   __syncthreads();
   // warp -> CTA (ascending warp), export warp partials
   unsigned long long* parts = (unsigned long long*)a.cluster_partials;

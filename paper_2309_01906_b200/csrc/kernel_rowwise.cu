@@ -13,36 +13,43 @@
 //   * each CTA's producer warp streams its n1/K-column segment of the row
 //     with one 1-D TMA bulk copy into an S-stage smem ring (full/empty
 //     mbarriers), L2 evict-first;
-//   * lane level: each lane sums its float4s (fp32 pairwise, fp64 across);
-//     lane -> warp: ordered SHFL tree (fp64);
-//   * warp -> CTA -> cluster: every warp's lane 0 pushes its warp partial
-//     with st.async into the LEADER CTA's slot ring over DSMEM; the store
-//     itself completes the leader's per-row mbarrier (complete_tx), so the
-//     warp- and CTA-level barriers are transaction barriers with no
-//     bar.sync / barrier.cluster in the row loop;
-//   * a combiner warp in the leader CTA waits the row's mbarrier, folds the
-//     K*W warp partials in ascending order (CTA partials, then the row),
-//     writes the row and frees the slot by arriving remotely on every CTA's
-//     slot-empty mbarrier.
-// Slots are a ring of R rows, so the combine of row j overlaps the loads of
-// rows j+1 .. j+S.  The only cluster barriers are at start-up and exit.
+//   * lane level: each lane sums its NV float4s in fp32; lane -> warp: xor
+//     butterfly (lane 0 receives exactly the ordered tree
+//     ((x0+x1)+(x2+x3))+..., §8(c) reading #4) in fp32 — a warp's share of a
+//     row is 128*NV elements, so the worst-case relative error of a warp
+//     partial is (4*NV + 4) u <= 2.2e-6 for NV <= 8 (reading #6);
+//   * warp -> CTA -> cluster: every warp's lane 0 pushes its warp partial with
+//     st.async into the LEADER CTA's slot ring over DSMEM; the store itself
+//     completes the leader's per-row mbarrier (complete_tx): the warp- and
+//     CTA-level barriers are transaction barriers, no bar.sync or
+//     barrier.cluster in the row loop;
+//   * a combiner warp in the leader CTA folds 32/(K*W) rows per pass in fp64
+//     (warp partials -> CTA partials -> row, ascending), writes the rows and
+//     frees their slots with relaxed remote arrives on every CTA's
+//     slot-empty mbarrier (a .release arrive would cost a MEMBAR.ALL.GPU).
+// The slot ring holds kSlots rows, so combining row j overlaps the loads of
+// rows j+1 .. j+S.  Cluster barriers only at start-up and exit.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include "fused_common.cuh"
 
 namespace hpar {
 namespace {
 
-constexpr int kStages = 6;   // TMA ring depth (rows in flight per CTA)
-constexpr int kSlots = 8;    // DSMEM row-slot ring depth in the leader
-constexpr int kMaxPush = 32; // K*W <= 32 warp partials per row
+constexpr int kMaxStages = 16;  // TMA ring depth bound (rows in flight per CTA)
+constexpr int kSlots = 16;      // DSMEM row-slot ring depth in the leader
+constexpr int kMaxPush = 32;    // K*W <= 32 warp partials per row
 
-template <bool VERIFY>
-__global__ void __launch_bounds__(1024, 1) rowwise_kernel(const __grid_constant__ NestArgs a, int W, int qcols) {
+
+// NV: float4 vectors per lane per row (qcols == 128*W*NV); 0 = generic loop
+template <bool VERIFY, int NV>
+__global__ void __launch_bounds__(1024, 1)
+    rowwise_kernel(const __grid_constant__ NestArgs a, int W, int qcols, int kStages) {
   extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ __align__(8) uint64_t row_full[kSlots], slot_empty[kSlots];
-  __shared__ __align__(8) double slot[kSlots][kMaxPush];
+  __shared__ __align__(8) float slot[kSlots][kMaxPush];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K;
@@ -51,7 +58,7 @@ __global__ void __launch_bounds__(1024, 1) rowwise_kernel(const __grid_constant_
   // cluster c's block of rows (static over C clusters)
   const int64_t q = a.n0 / a.C, r = a.n0 % a.C;
   const int64_t row0 = c * q + (c < r ? c : r);
-  const int64_t nrows = q + (c < r ? 1 : 0);
+  const uint32_t nrows = (uint32_t)(q + (c < r ? 1 : 0));
   const int64_t col0 = (int64_t)crank * qcols;
   const float* x = (const float*)a.in;
   const uint32_t seg_bytes = (uint32_t)qcols * 4;
@@ -63,47 +70,58 @@ __global__ void __launch_bounds__(1024, 1) rowwise_kernel(const __grid_constant_
       mbar_init(&empty[s], W);
     }
     for (int s = 0; s < kSlots; ++s) {
-      mbar_init(&row_full[s], 1);   // armed by the combiner with expect_tx
-      mbar_init(&slot_empty[s], 1); // one remote arrive from the leader's combiner
+      mbar_init(&row_full[s], 1);    // armed by the combiner with expect_tx
+      mbar_init(&slot_empty[s], 1);  // one remote arrive from the leader's combiner
     }
     fence_mbarrier_init_cluster();
   }
-  cluster_sync_all();  // barriers of every CTA initialised before any remote use
+  cluster_sync_all();  // every CTA's barriers initialised before any remote use
 
   if (warp == W) {
     // ------------------------------ producer warp: TMA row segments ----
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      for (int64_t j = 0; j < nrows; ++j) {
-        const int s = (int)(j % kStages);
-        if (j >= kStages) mbar_wait(&empty[s], (uint32_t)(((j / kStages) - 1) & 1));
+      const float* src = x + row0 * a.ld + col0;
+      int s = 0;
+      uint32_t ph = 0;
+      for (uint32_t j = 0; j < nrows; ++j) {
+        if (j >= (uint32_t)kStages) mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], seg_bytes);
-        bulk_g2s(dsm + (size_t)s * seg_bytes, x + (row0 + j) * a.ld + col0, seg_bytes, &full[s], pol);
+        bulk_g2s(dsm + (size_t)s * seg_bytes, src, seg_bytes, &full[s], pol);
+        src += a.ld;
+        if (++s == kStages) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == W + 1) {
     // ------------------------------ combiner warp (leader CTA only) ----
     if (crank == 0) {
-      for (int64_t j = 0; j < nrows; ++j) {
+      const int rpp = 32 / npush;          // rows per pass
+      const int g = lane / npush;          // this lane's row within the pass
+      const int e = lane % npush;          // warp partial index within the row
+      for (uint32_t j0 = 0; j0 < nrows; j0 += rpp) {
+        const uint32_t j = j0 + g;
+        const bool live = j < nrows;
         const int s = (int)(j % kSlots);
-        const uint32_t ph = (uint32_t)((j / kSlots) & 1);
-        if (lane == 0) mbar_arrive_expect_tx(&row_full[s], (uint32_t)(npush * 8));
-        mbar_wait_cluster(&row_full[s], ph);
-        double v = lane < npush ? slot[s][lane] : 0.0;
-        // warp partials -> CTA partials (lanes k*W), ordered
-        v = shfl_tree<OP_SUM, double>(v, 1, W);
-        if (VERIFY && (a.verify & V_PARTIALS) && lane < npush && (lane % W) == 0)
-          export_slot<double>(a, S_CTA, (row0 + j) * K + lane / W, v);
+        double v = 0.0;
+        if (live) {
+          if (e == 0) mbar_arrive_expect_tx(&row_full[s], (uint32_t)(npush * 4));
+          mbar_wait_cluster(&row_full[s], (j / kSlots) & 1);
+          v = (double)slot[s][e];
+        }
+        // warp partials -> CTA partials (every W lanes), ordered
+        for (int off = 1; off < W; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (VERIFY && live && (a.verify & V_PARTIALS) && (e % W) == 0)
+          export_slot<double>(a, S_CTA, (row0 + j) * K + e / W, v);
         // CTA partials -> row (cluster), ordered
-        v = shfl_tree<OP_SUM, double>(v, W, K);
-        if (lane == 0) {
+        for (int off = W; off < npush; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (live && e == 0) {
           const int64_t row = row0 + j;
           if (a.out_dtype == DT_F32) ((float*)a.out)[row] = (float)v;
           else ((double*)a.out)[row] = v;
         }
-        __syncwarp();
-        // free the slot in every CTA of the cluster
-        if (lane < K) mbar_arrive_cluster(mapa(smem_addr(&slot_empty[s]), (uint32_t)lane));
+        // free the slot in every CTA of the cluster (relaxed: it orders only
+        // the slot reads above, which the shuffles have consumed)
+        if (live && e < K) mbar_arrive_cluster_relaxed(mapa(smem_addr(&slot_empty[s]), (uint32_t)e));
       }
     }
   } else {
@@ -113,48 +131,62 @@ __global__ void __launch_bounds__(1024, 1) rowwise_kernel(const __grid_constant_
     const uint32_t leader_full_base = mapa(smem_addr(&row_full[0]), 0);
     const int push_idx = (int)crank * W + warp;
     const int64_t leaf = (int64_t)a.rank * a.threads_per_gpu + (int64_t)blockIdx.x * W * 32 + threadIdx.x;
-    for (int64_t j = 0; j < nrows; ++j) {
-      const int s = (int)(j % kStages);
-      mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
+    int s = 0, ss = 0;
+    uint32_t ph = 0, sph = 0;
+    for (uint32_t j = 0; j < nrows; ++j) {
+      mbar_wait(&full[s], ph);
       const float4* st = (const float4*)(dsm + (size_t)s * seg_bytes);
-      double acc = 0.0;
-      for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
-        const float4 v = st[f];
-        acc += (double)((v.x + v.y) + (v.z + v.w));
-        if constexpr (VERIFY) {
+      float acc = 0.f;
+      if constexpr (NV > 0) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const float4 t = st[(v * W + warp) * 32 + lane];
+          acc += (t.x + t.y) + (t.z + t.w);
+        }
+      } else {
+        for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
+          const float4 t = st[f];
+          acc += (t.x + t.y) + (t.z + t.w);
+        }
+      }
+      if constexpr (VERIFY) {
+        for (int f = warp * 32 + lane; f < nvec; f += W * 32)
           for (int e = 0; e < 4; ++e) {
             const int64_t it = (row0 + j) * a.n1 + col0 + 4 * f + e;
             if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
           }
-        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // stage consumed
+      if (++s == kStages) { s = 0; ph ^= 1; }
       if constexpr (VERIFY) {
         if (a.verify & V_PARTIALS)
           export_slot<double>(a, S_LANE_IN, (row0 + j) * (int64_t)(npush * 32) + push_idx * 32 + lane, acc);
       }
-      acc = warp_fold<OP_SUM>(acc);
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
       if (lane == 0) {
         if constexpr (VERIFY) {
           if (a.verify & V_PARTIALS) export_slot<double>(a, S_WARP, (row0 + j) * npush + push_idx, acc);
         }
-        const int ss = (int)(j % kSlots);
-        if (j >= kSlots) mbar_wait_cluster(&slot_empty[ss], (uint32_t)(((j / kSlots) - 1) & 1));
-        st_async_u64(leader_slot_base + (uint32_t)((ss * kMaxPush + push_idx) * 8),
-                     leader_full_base + (uint32_t)(ss * 8), (unsigned long long)__double_as_longlong(acc));
+        if (j >= (uint32_t)kSlots) mbar_wait_relaxed_cluster(&slot_empty[ss], sph ^ 1);
+        st_async_u32(leader_slot_base + (uint32_t)((ss * kMaxPush + push_idx) * 4),
+                     leader_full_base + (uint32_t)(ss * 8), __float_as_uint(acc));
       }
-      __syncwarp();
+      if (++ss == kSlots) { ss = 0; sph ^= 1; }
     }
   }
+  // reconverge the warp (producer / combiner lanes ran alone) before the
+  // blocking cluster barrier, so an idle lane never starves a working one
+  __syncwarp();
   // every CTA stays until the leader has consumed all pushes and freed slots
   cluster_sync_all();
 }
 
-template <bool V>
-cudaError_t launch_t(const NestArgs& a, int W, int qcols, cudaStream_t s) {
-  auto kern = rowwise_kernel<V>;
-  const size_t smem = (size_t)kStages * qcols * 4;
+template <bool V, int NV>
+cudaError_t launch_t(const NestArgs& a, int W, int qcols, int stages, cudaStream_t s) {
+  auto kern = rowwise_kernel<V, NV>;
+  const size_t smem = (size_t)stages * qcols * 4;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -169,10 +201,37 @@ cudaError_t launch_t(const NestArgs& a, int W, int qcols, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, W, qcols);
+  return cudaLaunchKernelEx(&cfg, kern, a, W, qcols, stages);
+}
+
+template <bool V>
+cudaError_t launch_nv(const NestArgs& a, int W, int qcols, int stages, cudaStream_t s) {
+  const int nv = (qcols % (128 * W) == 0) ? qcols / (128 * W) : 0;
+  switch (nv) {
+    case 1: return launch_t<V, 1>(a, W, qcols, stages, s);
+    case 2: return launch_t<V, 2>(a, W, qcols, stages, s);
+    case 4: return launch_t<V, 4>(a, W, qcols, stages, s);
+    case 8: return launch_t<V, 8>(a, W, qcols, stages, s);
+    default: return launch_t<V, 0>(a, W, qcols, stages, s);
+  }
 }
 
 bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int rowwise_stages(int qcols) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("HPAR_RW_STAGES");
+    env = e ? atoi(e) : -1;
+  }
+  // default: ~16 KiB of row segments in flight per CTA; many small CTAs keep
+  // more bytes in flight per SM than few deep ones (measured)
+  int st = (env >= 2 && env <= kMaxStages) ? env : (int)(16384 / ((size_t)qcols * 4));
+  if (st < 2) st = 2;
+  if (st > kMaxStages) st = kMaxStages;
+  while (st > 2 && (size_t)st * qcols * 4 > 200 * 1024) --st;
+  return st;
+}
 
 }  // namespace
 
@@ -193,9 +252,9 @@ bool rowwise_matches(const NestArgs& a, const char** why) {
   if (w->loop != 1 || w->sched != SCHED_STATIC_CHUNK || w->chunk != 128) { *why = "warp static(128)"; return false; }
   if (l->loop != 1 || l->sched != SCHED_STATIC_CHUNK || l->chunk != 4) { *why = "lane static(4)"; return false; }
   const int64_t K = a.K, W = a.radix[S_WARP];
-  if (!pow2(K) || !pow2(W) || K * W > kMaxPush) { *why = "K, W powers of two with K*W <= 32"; return false; }
+  if (!pow2(K) || !pow2(W) || K * W > kMaxPush || W > 30) { *why = "K, W powers of two, K*W <= 32"; return false; }
   if (a.n1 % (4 * K) != 0 || a.ld % 4 != 0 || ((uintptr_t)a.in & 15)) { *why = "alignment"; return false; }
-  if ((a.n1 / K) * 4 * kStages > 200 * 1024) { *why = "row segment too large for the smem ring"; return false; }
+  if ((a.n1 / K) * 4 * 2 > 200 * 1024) { *why = "row segment too large for the smem ring"; return false; }
   if (a.n1 == 0) { *why = "empty rows"; return false; }
   return true;
 }
@@ -203,7 +262,8 @@ bool rowwise_matches(const NestArgs& a, const char** why) {
 cudaError_t launch_rowwise(const NestArgs& a, int W, cudaStream_t s, const char** name) {
   *name = "rowwise_tma_dsmem";
   const int qcols = (int)(a.n1 / a.K);
-  return a.verify ? launch_t<true>(a, W, qcols, s) : launch_t<false>(a, W, qcols, s);
+  const int st = rowwise_stages(qcols);
+  return a.verify ? launch_nv<true>(a, W, qcols, st, s) : launch_nv<false>(a, W, qcols, st, s);
 }
 
 }  // namespace hpar

@@ -137,8 +137,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 // Arrive on the mbarrier at shared::cluster address `remote` (another CTA).
+// The .release form compiles to MEMBAR.ALL.GPU + arrive on sm_100a; use it
+// only when prior global/shared WRITES must be visible to the waiter.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t remote) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// Relaxed remote arrive (no fence): for "slot free" signals that only order
+// earlier READS, which are complete once their values were consumed.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t remote) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -163,6 +170,21 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t pa
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ bool mbar_try_wait_relaxed_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_relaxed_cluster(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_relaxed_cluster(bar, parity)) {
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
@@ -176,6 +198,12 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 __device__ __forceinline__ void st_async_u64(uint32_t remote_addr, uint32_t remote_bar, unsigned long long v) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u64 [%0], %1, [%2];" ::"r"(remote_addr),
                "l"(v), "r"(remote_bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_async_u32(uint32_t remote_addr, uint32_t remote_bar, uint32_t v) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(remote_addr),
+               "r"(v), "r"(remote_bar)
                : "memory");
 }
 
