@@ -7,8 +7,13 @@
 //     warp     static(512)       (32 lanes x 16 B)
 //     lane     static(16)
 // Privatisation per level:
-//     warp    : its own 256 u32 bins in shared memory (lanes increment them
-//               with shared-memory atomics — lanes have no private bins)
+//     lane    : its own 256 u32 counters, laid out counts[bin][lane] in the
+//               warp's shared-memory table, so lane l always hits bank l: no
+//               bank conflicts and no two lanes on one address, whatever the
+//               data (skewed or all-zero inputs cost the same).  Increments
+//               are fire-and-forget shared atomics (red.shared, no return
+//               value), so consecutive bytes of a lane never wait on each other.
+//     warp    : sum of its 32 lanes' counters (rotated reads, conflict-free)
 //     CTA     : sum of its warps' bins (ascending warp), bar.sync
 //     cluster : reduce-scatter over DSMEM — CTA k owns bins [256k/K, 256(k+1)/K)
 //               and sums them over the K CTAs (ascending), barrier.cluster
@@ -23,13 +28,19 @@
 namespace hpar {
 namespace {
 
-constexpr int kStages = 4;
+constexpr int kStages = 2;
+constexpr int kMaxW = 6;  // 6 x 32 KiB lane tables + the ring fit in 227 KiB
 
-template <bool VERIFY>
+__device__ __forceinline__ void inc_shared(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
+
+// VPL: 16-byte vectors per lane per tile (tile == 512*W*VPL), 0 = generic
+template <bool VERIFY, int VPL>
 __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ NestArgs a, int W, int tile) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  __shared__ uint32_t wbins[16][256];
+  __shared__ uint32_t wbins[kMaxW][256];
   __shared__ uint32_t cbins[256];
   __shared__ int s_flag;
 
@@ -43,8 +54,9 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
   const int K = a.K;
   const uint32_t crank = cluster_ctarank();
   const int64_t cl = blockIdx.x / K;
+  uint32_t* counts = (uint32_t*)(dsm + (size_t)kStages * tile);  // [W][256][32]
 
-  for (int i = threadIdx.x; i < W * 256; i += blockDim.x) (&wbins[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < W * 256 * 32; i += blockDim.x) counts[i] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -57,37 +69,67 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
   if (warp == W) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
       for (int64_t j = 0; j < my_tiles; ++j) {
-        const int s = (int)(j % kStages);
-        if (j >= kStages) mbar_wait(&empty[s], (uint32_t)(((j / kStages) - 1) & 1));
+        if (j >= kStages) mbar_wait(&empty[s], ph ^ 1);
         const int64_t base = (j * nblocks + b) * tile;
         const int64_t len = (n - base < tile) ? (n - base) : tile;
         const uint32_t bytes = (uint32_t)(len & ~(int64_t)15);
         mbar_arrive_expect_tx(&full[s], bytes);
         if (bytes) bulk_g2s(dsm + (size_t)s * tile, x + base, bytes, &full[s], pol);
+        if (++s == kStages) { s = 0; ph ^= 1; }
       }
     }
   } else {
-    uint32_t* mybins = wbins[warp];
+    // this lane's column of the warp's table: word (bin*32 + lane)
+    const uint32_t col = smem_addr(counts + (size_t)warp * 256 * 32 + lane);
     const int nvec = tile / 16;
     const int64_t leaf = (int64_t)a.rank * a.threads_per_gpu + b * W * 32 + threadIdx.x;
+    int s = 0;
+    uint32_t ph = 0;
     for (int64_t j = 0; j < my_tiles; ++j) {
-      const int s = (int)(j % kStages);
       const int64_t base = (j * nblocks + b) * tile;
       const int64_t len = (n - base < tile) ? (n - base) : tile;
-      mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
+      mbar_wait(&full[s], ph);
       const unsigned char* st = dsm + (size_t)s * tile;
-      if (len == tile) {
+      if (len == tile && VPL > 0) {
+        // all of this lane's vectors of the tile first (ILP over the smem
+        // latency), then the increments
+        uint4 vv[VPL > 0 ? VPL : 1];
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) vv[q] = ((const uint4*)st)[(q * W + warp) * 32 + lane];
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const uint32_t w4[4] = {vv[q].x, vv[q].y, vv[q].z, vv[q].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t w = w4[k];
+            inc_shared(col + ((w << 7) & 0x7F80u));   // byte 0 -> bin*128
+            inc_shared(col + ((w >> 1) & 0x7F80u));   // byte 1
+            inc_shared(col + ((w >> 9) & 0x7F80u));   // byte 2
+            inc_shared(col + ((w >> 17) & 0x7F80u));  // byte 3
+          }
+        }
+        if constexpr (VERIFY) {
+          for (int f = warp * 32 + lane; f < nvec; f += W * 32)
+            for (int e = 0; e < 16; ++e) {
+              const int64_t it = base + 16 * f + e;
+              if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
+            }
+        }
+      } else if (len == tile) {
 #pragma unroll 2
         for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
           const uint4 v = ((const uint4*)st)[f];
           const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            atomicAdd(&mybins[w4[k] & 0xFF], 1u);
-            atomicAdd(&mybins[(w4[k] >> 8) & 0xFF], 1u);
-            atomicAdd(&mybins[(w4[k] >> 16) & 0xFF], 1u);
-            atomicAdd(&mybins[w4[k] >> 24], 1u);
+            const uint32_t w = w4[k];
+            inc_shared(col + ((w << 7) & 0x7F80u));   // byte 0 -> bin*128
+            inc_shared(col + ((w >> 1) & 0x7F80u));   // byte 1
+            inc_shared(col + ((w >> 9) & 0x7F80u));   // byte 2
+            inc_shared(col + ((w >> 17) & 0x7F80u));  // byte 3
           }
           if constexpr (VERIFY) {
             for (int e = 0; e < 16; ++e) {
@@ -102,8 +144,8 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
           for (int e = 0; e < 16; ++e) {
             const int64_t off = 16 * (int64_t)f + e;
             if (off >= len) break;
-            const uint8_t byte = off < in_smem ? st[off] : x[base + off];
-            atomicAdd(&mybins[byte], 1u);
+            const uint32_t byte = off < in_smem ? st[off] : x[base + off];
+            inc_shared(col + (byte << 7));
             if constexpr (VERIFY) {
               if (a.verify & V_COVERAGE) { a.owner[base + off] = leaf; atomicAdd(&a.count[base + off], 1u); }
             }
@@ -112,22 +154,41 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == kStages) { s = 0; ph ^= 1; }
     }
   }
   __syncwarp();
   __syncthreads();
-  // warp -> CTA (ascending warp), export warp partials
+  // lane -> warp: warp w sums the 32 lane columns of its table; lane l owns
+  // bins l, l+32, ...; rotated column order keeps the reads conflict-free
+  if (warp < W) {
+    const uint32_t* tab = counts + (size_t)warp * 256 * 32;
+    for (int bin = lane; bin < 256; bin += 32) {
+      uint32_t sacc = 0;
+      for (int k = 0; k < 32; ++k) {
+        const int l = (k + lane) & 31;
+        const uint32_t v = tab[bin * 32 + l];
+        sacc += v;
+        if (VERIFY && (a.verify & V_PARTIALS)) {
+          for (int lv = 0; lv < a.nlev; ++lv)
+            if (a.lv[lv].slast == S_LANE_IN && a.partials[lv])
+              ((unsigned long long*)a.partials[lv])[((int64_t)blockIdx.x * W * 32 + warp * 32 + l) * 256 + bin] = v;
+        }
+      }
+      wbins[warp][bin] = sacc;
+      if (VERIFY && (a.verify & V_PARTIALS)) {
+        for (int lv = 0; lv < a.nlev; ++lv)
+          if (a.lv[lv].slast == S_WARP && a.partials[lv])
+            ((unsigned long long*)a.partials[lv])[((int64_t)blockIdx.x * W + warp) * 256 + bin] = sacc;
+      }
+    }
+  }
+  __syncthreads();
+  // warp -> CTA (ascending warp)
   unsigned long long* parts = (unsigned long long*)a.cluster_partials;
   for (int bin = threadIdx.x; bin < 256; bin += blockDim.x) {
     uint32_t sacc = 0;
-    for (int w = 0; w < W; ++w) {
-      sacc += wbins[w][bin];
-      if (VERIFY && (a.verify & V_PARTIALS)) {
-        for (int l = 0; l < a.nlev; ++l)
-          if (a.lv[l].slast == S_WARP && a.partials[l])
-            ((unsigned long long*)a.partials[l])[((int64_t)blockIdx.x * W + w) * 256 + bin] = wbins[w][bin];
-      }
-    }
+    for (int w = 0; w < W; ++w) sacc += wbins[w][bin];
     cbins[bin] = sacc;
     if (VERIFY && (a.verify & V_PARTIALS)) {
       for (int l = 0; l < a.nlev; ++l)
@@ -178,10 +239,10 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
   }
 }
 
-template <bool V>
+template <bool V, int VPL>
 cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
-  auto kern = hist_kernel<V>;
-  const size_t smem = (size_t)kStages * tile;
+  auto kern = hist_kernel<V, VPL>;
+  const size_t smem = (size_t)kStages * tile + (size_t)W * 256 * 32 * 4;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -218,14 +279,21 @@ bool hist_matches(const NestArgs& a, const char** why) {
   if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 512) { *why = "warp static(512)"; return false; }
   if (k->sched != SCHED_STATIC_CHUNK || tile % (512 * W) != 0 || tile > 32768) { *why = "CTA static(tile)"; return false; }
   if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster static(K*tile)"; return false; }
-  if (W > 16) { *why = "W <= 16 (warp bins)"; return false; }
+  if (W > kMaxW || kStages * tile + W * 32768 > 227 * 1024) { *why = "W <= 6 (32 KiB lane tables per warp)"; return false; }
   return true;
 }
 
 cudaError_t launch_hist(const NestArgs& a, int W, cudaStream_t s, const char** name) {
-  *name = "hist256_tma";
+  *name = "hist256_lanepriv_tma";
   const int tile = (int)device_levels(a).l[1]->chunk;
-  return a.verify ? launch_t<true>(a, W, tile, s) : launch_t<false>(a, W, tile, s);
+  const int vpl = (tile % (512 * W) == 0) ? tile / (512 * W) : 0;
+  if (a.verify) return vpl == 8 ? launch_t<true, 8>(a, W, tile, s) : launch_t<true, 0>(a, W, tile, s);
+  switch (vpl) {
+    case 4: return launch_t<false, 4>(a, W, tile, s);
+    case 8: return launch_t<false, 8>(a, W, tile, s);
+    case 16: return launch_t<false, 16>(a, W, tile, s);
+    default: return launch_t<false, 0>(a, W, tile, s);
+  }
 }
 
 }  // namespace hpar

@@ -312,11 +312,11 @@ def test_hist_fused_kernel(H, torch_mod, oracle, n):
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     levels = nests.c4_nest(K=2)
-    C, K, W = 5, 2, 8
+    C, K, W = 5, 2, 4
     for x in (gen.gen_u8(gen.SEED_C4, 0, n), gen.gen_u8_zipf(gen.SEED_C4, 0, n), np.zeros(n, np.uint8)):
         res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, coverage=n <= 200000,
                        partials=n <= 200000)
-        assert res["kernel"] == "hist256_tma"
+        assert res["kernel"] == "hist256_lanepriv_tma"
         assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
         if n <= 200000:
             compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
