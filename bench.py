@@ -116,6 +116,7 @@ def config_spec(name: str, nranks: int):
                     seed=gen.SEED_C1, dtype="i32", elems_per_rank=1 << 20, bytes_per_rank=(1 << 22) + 8)
     if name == "c3":
         return dict(workload="c3_csr_segmented_2^24rows_2^28nnz_f32", kind="csr", rows=1 << 24, nnz=1 << 28,
+                    n0=(1 << 24) * nranks,
                     scaling="weak", seed=gen.SEED_C3, dtype="f32", elems_per_rank=1 << 28,
                     bytes_per_rank=(1 << 30) + ((1 << 24) + 1) * 8 + (1 << 24) * 4)
     raise SystemExit(f"unknown config {name}")
@@ -161,6 +162,7 @@ def run_hpar(args):
     if args.clusters < 0:
         args.clusters = tuned[1]
     kind = spec["kind"]
+    extra_inputs = []
     if kind == "rowwise":
         nest = H.Nest(nests.c2_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
                       clusters=args.clusters)
@@ -206,8 +208,23 @@ def run_hpar(args):
         elems_rank = cnt * 1024
         alg_bytes = cnt * 1024 * 4 + 8
         host_in_bytes, host_out_bytes = cnt * 4096, 8
-    else:
-        raise SystemExit("config c3 is not wired into bench.py yet")
+    else:  # c3: CSR segmented rows
+        from inputs import gen
+        rows, nnz = spec["rows"], spec["nnz"]
+        off_host = gen.csr_offsets(rows, nnz)
+        nest = H.Nest(nests.c3_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+                      clusters=args.clusters)
+        b, cnt = nest.shard_range(rows * world, rank)  # each rank: its own copy of the matrix (weak)
+        off = torch.from_numpy(off_host).to(dev)
+        x = torch.empty(nnz, dtype=torch.float32, device=dev)
+        L.hpar_inputs_fill_f32(spec["seed"], rank * nnz, nnz, x.data_ptr(), sptr)
+        out = torch.empty(rows, dtype=torch.float32, device=dev)
+        desc = H.make_desc(x, out, n0=rows * world, nloops=2, keyed=True, offsets=off,
+                           max_inner=int((off_host[1:] - off_host[:-1]).max()))
+        elems_rank = nnz
+        alg_bytes = nnz * 4 + (rows + 1) * 8 + rows * 4
+        host_in_bytes, host_out_bytes = nnz * 4 + (rows + 1) * 8, rows * 4
+        extra_inputs = [off]
     torch.cuda.synchronize()
 
     def step():
@@ -262,8 +279,12 @@ def run_hpar(args):
     e2e = None
     if not args.no_e2e:
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
-        host_x = torch.empty(x.numel(), dtype=x.dtype, pin_memory=True)
-        host_x.copy_(x)
+        dev_inputs = [x] + extra_inputs
+        host_inputs = []
+        for t_ in dev_inputs:
+            h_ = torch.empty(t_.numel(), dtype=t_.dtype, pin_memory=True)
+            h_.copy_(t_)
+            host_inputs.append(h_)
         host_out = torch.empty(out.numel(), dtype=out.dtype, pin_memory=True)
         torch.cuda.synchronize()
         if world > 1:
@@ -272,7 +293,8 @@ def run_hpar(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e2e_steps):
-            x.copy_(host_x, non_blocking=True)
+            for d_, h_ in zip(dev_inputs, host_inputs):
+                d_.copy_(h_, non_blocking=True)
             step()
             host_out.copy_(out, non_blocking=True)
         e1.record(stream)
