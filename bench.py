@@ -212,14 +212,14 @@ def run_hpar(args):
         from inputs import gen
         rows, nnz = spec["rows"], spec["nnz"]
         off_host = gen.csr_offsets(rows, nnz)
-        nest = H.Nest(nests.c3_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+        nest = H.Nest(nests.c3_fast_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
                       clusters=args.clusters)
         b, cnt = nest.shard_range(rows * world, rank)  # each rank: its own copy of the matrix (weak)
         off = torch.from_numpy(off_host).to(dev)
         x = torch.empty(nnz, dtype=torch.float32, device=dev)
         L.hpar_inputs_fill_f32(spec["seed"], rank * nnz, nnz, x.data_ptr(), sptr)
         out = torch.empty(rows, dtype=torch.float32, device=dev)
-        desc = H.make_desc(x, out, n0=rows * world, nloops=2, keyed=True, offsets=off,
+        desc = H.make_desc(x, out, n0=rows * world, n1=nnz, nloops=2, keyed=True, offsets=off,
                            max_inner=int((off_host[1:] - off_host[:-1]).max()))
         elems_rank = nnz
         alg_bytes = nnz * 4 + (rows + 1) * 8 + rows * 4

@@ -33,6 +33,10 @@ cudaError_t launch_rowwise(const NestArgs& a, int W, cudaStream_t s, const char*
 bool hist_matches(const NestArgs& a, const char** why);
 cudaError_t launch_hist(const NestArgs& a, int W, cudaStream_t s, const char** name);
 int flat_resident_ctas_per_sm(int W);
+bool segmented_matches(const NestArgs& a, const char** why);
+cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaStream_t s, const char** name);
+size_t segmented_ws_bytes(int64_t nnz);
+void segmented_ws_qrow(int64_t nnz, size_t* off, size_t* len);
 }  // namespace hpar
 
 using namespace hpar;
@@ -247,6 +251,8 @@ struct hpar_nest {
   int32_t* error_flag = nullptr;
   int* barrier_word = nullptr;
   std::string last_kernel = "none";
+  void* seg_ws = nullptr;  // CSR segmented kernel workspace (grown on demand)
+  size_t seg_ws_bytes = 0;
 };
 
 namespace {
@@ -307,7 +313,7 @@ extern "C" hpar_status hpar_nest_create(const hpar_nest_level* lv, int32_t nleve
     n->user[a] = L;
     if (L.first < HPAR_GPU || L.last > HPAR_LANE || L.first > L.last)
       return bail(fail(HPAR_E_INVALID, "nest level %d: hardware range [%d,%d] outside gpu..lane", a, L.first, L.last));
-    if (L.loop != 0 && L.loop != 1) return bail(fail(HPAR_E_INVALID, "nest level %d: loop must be 0 or 1", a));
+    if (L.loop < 0 || L.loop > 2) return bail(fail(HPAR_E_INVALID, "nest level %d: loop must be 0, 1 or 2", a));
     if (L.schedule < 0 || L.schedule > 3) return bail(fail(HPAR_E_INVALID, "nest level %d: bad schedule", a));
     if ((L.schedule == HPAR_SCHED_STATIC_CHUNK || L.schedule == HPAR_SCHED_DYNAMIC) && L.chunk < 1)
       return bail(fail(HPAR_E_INVALID, "nest level %d: %s needs chunk >= 1", a, sched_name(L.schedule)));
@@ -477,6 +483,7 @@ extern "C" hpar_status hpar_nest_destroy(hpar_nest_t n) {
     cudaFree(n->dyn_tickets);
     cudaFree(n->error_flag);
     cudaFree(n->barrier_word);
+    cudaFree(n->seg_ws);
   }
   delete n;
   return ok();
@@ -574,10 +581,17 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   if (d->nloops != 1 && d->nloops != 2) return fail(HPAR_E_INVALID, "nloops must be 1 or 2");
   if (d->n0 < 0 || d->n1 < 0) return fail(HPAR_E_INVALID, "negative loop extent");
   if (!d->out) return fail(HPAR_E_INVALID, "out is NULL");
-  for (int a = 0; a < n->nlev; ++a)
-    if (n->lv[a].loop >= d->nloops)
+  bool collapsed = false;  // a level bound to loop 2: the flattened (row, column) space
+  for (int a = 0; a < n->nlev; ++a) {
+    if (n->lv[a].loop == 2) {
+      collapsed = true;
+      if (d->nloops != 2)
+        return fail(HPAR_E_INVALID, "nest level %d binds the collapsed loop 2 but the call has one loop", a);
+    } else if (n->lv[a].loop >= d->nloops) {
       return fail(HPAR_E_INVALID, "nest level %d binds loop %d but the call has %d loop(s)", a, n->lv[a].loop,
                   d->nloops);
+    }
+  }
   const bool csr = d->nloops == 2 && d->offsets != nullptr;
   if (d->nloops == 2 && !csr && d->ld < d->n1) return fail(HPAR_E_INVALID, "ld < n1");
   if (d->keyed && d->nloops != 2) return fail(HPAR_E_INVALID, "keyed results need two loops");
@@ -591,6 +605,7 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   for (int a = 0; a < n->nlev; ++a) {
     if (n->lv[a].sched != SCHED_NONE) continue;
     const int loop = n->lv[a].loop;
+    if (loop == 2) return fail(HPAR_E_UNSUPPORTED, "nest level %d: schedule(none) over the collapsed loop", a);
     int64_t extent = loop == 0 ? d->n0 : d->n1;
     if (loop == 1 && csr) {
       if (d->max_inner <= 0)
@@ -667,7 +682,7 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
     int k = 0;
     while (k < n->nlev && n->lv[k].loop == 0) ++k;
     for (int a = k; a < n->nlev; ++a)
-      if (n->lv[a].loop != 1)
+      if (n->lv[a].loop == 0)
         return fail(HPAR_E_INVALID, "keyed results: the levels bound to loop 0 must be the outermost ones");
     if (k == 0) return fail(HPAR_E_UNSUPPORTED, "keyed results need loop 0 bound to an outer level");
     A.first_inner = k;
@@ -699,6 +714,25 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
     e = launch_flat(A, (int)n->W, stream, &name);
   } else if (rowwise_matches(A, &why)) {
     e = launch_rowwise(A, (int)n->W, stream, &name);
+  } else if (segmented_matches(A, &why)) {
+    // CSR: n1 = nonzeros of this rank's shard (local offsets start at 0)
+    const int64_t nnz = d->n1;
+    const size_t need = segmented_ws_bytes(nnz);
+    if (need > n->seg_ws_bytes) {
+      cudaFree(n->seg_ws);
+      n->seg_ws = nullptr;
+      n->seg_ws_bytes = 0;
+      cudaError_t ae = cudaMalloc(&n->seg_ws, need);
+      if (ae != cudaSuccess) return fail(HPAR_E_NOMEM, "segmented workspace (%zu B): %s", need, cudaGetErrorString(ae));
+      size_t qoff, qlen;
+      segmented_ws_qrow(nnz, &qoff, &qlen);
+      CUDA_TRY(cudaMemsetAsync(n->seg_ws, 0, need, stream));
+      CUDA_TRY(cudaMemsetAsync((char*)n->seg_ws + qoff, 0xFF, qlen, stream));  // empty queue slots = -1
+      n->seg_ws_bytes = need;
+    }
+    e = launch_segmented(A, n->seg_ws, nnz, stream, &name);
+  } else if (collapsed) {
+    return fail(HPAR_E_UNSUPPORTED, "collapsed loop 2: only the CSR segmented nest shape is implemented (%s)", why);
   } else {
     // generic interpreter: at most one dynamic level, on loop 0
     int ndyn = 0;

@@ -77,5 +77,20 @@ def c3_nest(with_gpu: bool = True, rows_chunk: int = 64, width: int = 8) -> list
     return lv
 
 
-__all__ = ["c1_nest", "c2_nest", "c3_nest", "c4_nest", "c5_nest", "flat_nest", "TILE_F32", "TILE_U8",
+def c3_fast_nest(with_gpu: bool = True, rows_chunk: int = 128) -> list[Level]:
+    """Config 3 (the fused CSR kernel's nest): rows (loop 0) dynamic(rows_chunk)
+    over ALL warps of the GPU (cluster..warp collapsed: flags = intersection,
+    dynamic and atomic hold); the block's nonzeros (loop 2 = the collapsed
+    (row, nonzero) space) static(8) over the lanes.  Rows longer than
+    1024 nonzeros are re-bound by length class to dynamic(8192) segments over
+    the warps (kernel_segmented.cu; reading #14)."""
+    lv = []
+    if with_gpu:
+        lv.append(Level(HPAR_GPU, HPAR_GPU, STATIC, loop=0))
+    lv += [Level(HPAR_CLUSTER, HPAR_WARP, DYNAMIC, loop=0, chunk=rows_chunk),
+           Level(HPAR_LANE, HPAR_LANE, STATIC_CHUNK, loop=2, chunk=8)]
+    return lv
+
+
+__all__ = ["c3_fast_nest","c1_nest", "c2_nest", "c3_nest", "c4_nest", "c5_nest", "flat_nest", "TILE_F32", "TILE_U8",
            "NONE"]

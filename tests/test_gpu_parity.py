@@ -322,6 +322,55 @@ def test_hist_fused_kernel(H, torch_mod, oracle, n):
             compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
 
 
+def _csr_cases():
+    off_z = gen.csr_offsets(3000, 40000)
+    yield "zipf", off_z
+    yield "all_empty", np.zeros(501, dtype=np.int64)
+    yield "one_huge_row", np.array([0, (1 << 20) + 3], dtype=np.int64)
+    lens = np.array([0, 1, 0, 0, 1024, 1025, 0, 3, 2048 + 5, 0, 0, 127, 128, 129, 0, 8192, 8193, 1, 0],
+                    dtype=np.int64)
+    lens = np.tile(lens, 20)
+    off = np.zeros(lens.size + 1, dtype=np.int64)
+    off[1:] = np.cumsum(lens)
+    yield "edges", off
+    yield "short_only", np.arange(0, 2 * 70001, 2, dtype=np.int64)
+
+
+@pytest.mark.parametrize("case", ["zipf", "all_empty", "one_huge_row", "edges", "short_only"])
+def test_segmented_csr_kernel(H, torch_mod, oracle, case):
+    """Config-3 fused kernel: every row sum within 1e-5 of the oracle's fp64
+    segment sums (0 exactly for empty rows), every nonzero visited once, each
+    block of 128 rows' short rows handled by one warp (dynamic chunk alignment)."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    off = dict(_csr_cases())[case]
+    rows, nnz = off.size - 1, int(off[-1])
+    v = gen.gen_f32(gen.SEED_C3, 0, nnz)
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=5)
+    xd = torch.from_numpy(v).cuda() if nnz else torch.zeros(4, dtype=torch.float32, device="cuda")
+    offd = torch.from_numpy(off).cuda()
+    out = torch.full((max(rows, 1),), -1.0, dtype=torch.float64, device="cuda")
+    owner = torch.full((max(nnz, 1),), -1, dtype=torch.int64, device="cuda")
+    count = torch.zeros(max(nnz, 1), dtype=torch.int32, device="cuda")
+    for verify in (0, H.VERIFY_COVERAGE):
+        out.fill_(-1.0)
+        d = H.make_desc(xd, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd, out_dtype=H.F64,
+                        verify=verify, owner=owner if verify else None, count=count if verify else None)
+        nest.parallel_for_reduce(d)
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "segmented_csr"
+        assert_rel(out.cpu().numpy()[:rows], oracle.segsum_f32(v, off))
+    if nnz:
+        assert (count.cpu().numpy()[:nnz] == 1).all()
+        own = owner.cpu().numpy()[:nnz] // 32  # warp of the owner
+        lens = np.diff(off)
+        for b0 in range(0, rows, 128):
+            rs = [r for r in range(b0, min(b0 + 128, rows)) if 0 < lens[r] <= 1024]
+            if rs:
+                ws_ = np.concatenate([own[off[r]:off[r + 1]] for r in rs])
+                assert (ws_ == ws_[0]).all(), "a block's short rows span several warps"
+
+
 def test_barrier_probes(H, torch_mod):
     """§8(a) A10: lane / warp / CTA barriers give rendezvous + visibility
     (0 mismatches); the cluster level has no barrier."""
