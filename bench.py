@@ -25,6 +25,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -392,26 +394,66 @@ def cpu_baseline(config: str, budget_s: float = 10.0, samples: int = 1):
     return None
 
 
+def oracle_step_fn(config: str, n_elems: int):
+    """(callable, elements per call, description): the oracle's plain
+    definition over a bounded sample of the config's workload."""
+    from inputs import gen
+    from oracle import oracle as O
+    O.build()
+    if config == "c2":
+        cols = 4096
+        rows = max(1, min(65536, n_elems // cols))
+        a = gen.gen_f32(gen.SEED_C2, 0, rows * cols)
+        return (lambda: O.rowsum_f32(a, rows, cols)), rows * cols, f"or_rowsum_f32 over rows [0,{rows}) x 4096"
+    if config == "c3":
+        off = gen.csr_offsets(1 << 24, 1 << 28)
+        rows = int(np.searchsorted(off, min(n_elems, 1 << 28))) if n_elems else 1
+        rows = max(1, min(1 << 24, rows))
+        nnz = int(off[rows])
+        v = gen.gen_f32(gen.SEED_C3, 0, nnz)
+        o = off[: rows + 1].copy()
+        return (lambda: O.segsum_f32(v, o)), nnz, f"or_segsum_f32 over rows [0,{rows}) ({nnz} nonzeros)"
+    n = max(1024, n_elems)
+    if config == "c4":
+        x = gen.gen_u8(gen.SEED_C4, 0, n)
+        return (lambda: O.hist256(x)), n, f"or_hist256 over bytes [0,{n})"
+    if config == "c1":
+        x = gen.gen_i32(gen.SEED_C1, 0, n)
+        return (lambda: O.sum_i32(x)), n, f"or_sum_i32 over elements [0,{n})"
+    x = gen.gen_f32(gen.SEED_C5, 0, n)
+    return (lambda: O.sum_f32(x)), n, f"or_sum_f32 over elements [0,{n})"
+
+
 def run_reference(args):
+    """The reference arm of this tier: the CPU oracle as it stands, one core,
+    W untimed + K timed steps, each step a bounded sample of the workload
+    (sized so the whole run takes about a minute)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # one step = the oracle over a bounded sample of the workload, sized so the
-    # whole --warmup + --steps run ends within ~2 minutes
-    total_budget = 120.0
-    per_step = max(0.01, total_budget / max(1, args.steps + args.warmup))
-    base = cpu_baseline(args.config, budget_s=min(per_step, 10.0))
     spec = config_spec(args.config, 1)
-    value = base["value"]
-    elems_step = value * per_step
+    f, n, _ = oracle_step_fn(args.config, 1 << 20)
+    t0 = time.perf_counter()
+    f()
+    per_elem = (time.perf_counter() - t0) / n
+    target = min(10.0, 60.0 / max(1, args.steps + args.warmup))
+    f, n, what = oracle_step_fn(args.config, int(target / max(per_elem, 1e-12)))
+    for _ in range(args.warmup):
+        f()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        f()
+    dt = time.perf_counter() - t0
+    value = n * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": elems_step / value * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": spec["scaling"], "vs_baseline": None, "dtype": spec["dtype"],
         "data": "synthetic (seeded splitmix64, inputs/gen.py recipe)",
         "config": {"workload": spec["workload"], "kernel": "oracle (CPU, sequential C)"},
-        "cpu_baseline": base,
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{what} per step, {args.steps} timed steps, {dt:.1f} s"},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -420,7 +462,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="hpar", choices=["hpar", "reference"])
