@@ -1,10 +1,10 @@
 # ncu evidence for the fused kernels (run under gpurun; one GPU)
 mkdir -p gpurun_out
-set -x
-for c in c2 c5 c4; do
+for spec in "c2:rowwise" "c5:flat_tma" "c4:hist" "c3:segmented" "c1:generic"; do
+  c=${spec%%:*}; k=${spec##*:}
   CMD="python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
-  $CMD > gpurun_out/plain_$c.log 2>&1 || continue
+  $CMD > gpurun_out/plain_$c.log 2>&1 || { echo "plain $c failed"; continue; }
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 12 --csv --log-file gpurun_out/launches_$c.csv $CMD > /dev/null 2>&1
-  ncu --set full --clock-control none --import-source on -k regex:"rowwise|flat_tma|hist" -s 3 -c 1 -o gpurun_out/prof_$c $CMD > gpurun_out/ncu_$c.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"$k" -s 3 -c 1 -o gpurun_out/prof_$c $CMD > gpurun_out/ncu_$c.log 2>&1
+  echo "$c ncu=$?"
 done
-ls -la gpurun_out
