@@ -37,6 +37,8 @@ bool segmented_matches(const NestArgs& a, const char** why);
 cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaStream_t s, const char** name);
 size_t segmented_ws_bytes(int64_t nnz);
 void segmented_ws_qrow(int64_t nnz, size_t* off, size_t* len);
+bool teams_matches(const NestArgs& a, const char** why);
+cudaError_t launch_teams(const NestArgs& a, int W, cudaStream_t s, const char** name);
 }  // namespace hpar
 
 using namespace hpar;
@@ -731,6 +733,8 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
       n->seg_ws_bytes = need;
     }
     e = launch_segmented(A, n->seg_ws, nnz, stream, &name);
+  } else if (teams_matches(A, &why)) {
+    e = launch_teams(A, (int)n->W, stream, &name);
   } else if (collapsed) {
     return fail(HPAR_E_UNSUPPORTED, "collapsed loop 2: only the CSR segmented nest shape is implemented (%s)", why);
   } else {

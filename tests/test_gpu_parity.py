@@ -157,6 +157,7 @@ def test_c1_generic_bit_exact(H, torch_mod, oracle):
     C, K, W = 512, 2, 8
     res = run_nest(H, torch, levels, x, n0=1024, n1=1024, C=C, K=K, W=W)
     assert res["out"][0] == oracle.sum_i32(x)
+    assert res["kernel"] == "teams_threads"
     compare(oracle, H, levels, res, x, n0=1024, n1=1024, C=C, K=K, W=W)
 
 
