@@ -182,7 +182,8 @@ def run_hpar(args):
             nest = H.Nest(nests.c5_nest(K), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
                           clusters=args.clusters)
         else:
-            nest = H.Nest(nests.c4_nest(K), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+            nest = H.Nest(nests.c4_nest(K, tile=int(os.environ.get("HPAR_C4_TILE", nests.TILE_U8))),
+                          device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
                           clusters=args.clusters)
         b, cnt = nest.shard_range(spec["n0"], rank)
         if kind == "flat":

@@ -28,7 +28,7 @@
 namespace hpar {
 namespace {
 
-constexpr int kStages = 2;
+constexpr int kStages = 5;  // 5 x 16 KiB in flight per CTA next to 4 x 32 KiB lane tables
 constexpr int kMaxW = 6;  // 6 x 32 KiB lane tables + the ring fit in 227 KiB
 
 __device__ __forceinline__ void inc_shared(uint32_t addr) {

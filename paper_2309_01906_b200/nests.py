@@ -45,8 +45,8 @@ def c5_nest(K: int = 2, with_gpu: bool = True) -> list[Level]:
     return flat_nest(K, TILE_F32, 4, with_gpu)
 
 
-def c4_nest(K: int = 2, with_gpu: bool = True) -> list[Level]:
-    return flat_nest(K, TILE_U8, 16, with_gpu)
+def c4_nest(K: int = 2, with_gpu: bool = True, tile: int = TILE_U8) -> list[Level]:
+    return flat_nest(K, tile, 16, with_gpu)
 
 
 def c2_nest(with_gpu: bool = True) -> list[Level]:
