@@ -22,12 +22,13 @@
 // Empty rows write 0.  Results are deterministic (fixed trees and orders).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include "fused_common.cuh"
 
 namespace hpar {
 namespace {
 
-constexpr int RB = 128;         // rows per block claim
+constexpr int RB = 256;         // rows per block claim
 constexpr int64_t LONG = 1024;  // a row with more nonzeros is split
 constexpr int64_t SEG = 8192;   // nonzeros per long-row segment
 constexpr int WARPS = 8;        // warps per CTA (all workers)
@@ -36,7 +37,7 @@ constexpr int WIN = 128 * NV;   // nonzeros per window (lane l: 4*NV contiguous 
 constexpr int LPL = 4 * NV;     // nonzeros per lane per window
 constexpr int D = 4;            // window prefetch depth (cp.async ring)
 constexpr int LBIT = 1 << 30;   // row-id flag: a long row (its nonzeros are phase 2's)
-constexpr int CB = 8;           // row blocks per CTA claim (CTA-level dynamic chunk)
+constexpr int CB = 32;          // row blocks per CTA claim (CTA-level dynamic chunk)
 constexpr int NSB = 8;          // ring of claimed CTA chunks
 
 struct CtaSmem {
@@ -92,7 +93,7 @@ __device__ __forceinline__ void seg_scan(int& row, float& v) {
 }
 
 template <bool VERIFY, bool OUT_F32>
-__global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws) {
+__global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg) {
   extern __shared__ __align__(16) unsigned char seg_dsm[];
   __shared__ CtaSmem cs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     }
     return t;
   };
+  unsigned long long my_blocks = 0;  // added to blocks_done once, when this warp leaves phase 1
   unsigned long long u = claim();
   load_offs(u);
   while ((int64_t)u < nblocks) {
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     int slot = 0;
 #pragma unroll
     for (int i = 0; i < D; ++i) issue(WIN * i, i);
-    for (int wr = 0; wr < p1; wr += WIN) {
+    for (int wr = (dbg & 2) ? p1 : 0; wr < p1; wr += WIN) {
       // inside a long row with no head ahead in this window: skip to the window
       // holding the next row start (the long row's nonzeros are phase 2's)
       if (open_row >= 0 && (open_row & LBIT)) {
@@ -326,11 +328,14 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     // the last open row of the block ends at P1
     if (lane == 0 && open_row >= 0 && !(open_row & LBIT)) write_row(r0 + open_row, carry);
     __syncwarp();
-    if (lane == 0) {
-      if (had_long) __threadfence();  // queue entries visible before blocks_done says so
-      atomicAdd(ws.blocks_done, 1ull);
-    }
+    if (had_long && lane == 0) __threadfence();  // queue entries visible before blocks_done says so
+    ++my_blocks;
     u = u1;
+  }
+
+  if (lane == 0) {
+    __threadfence();
+    atomicAdd(ws.blocks_done, my_blocks);
   }
 
   // -------------------------------------------- phase 2: long-row segments ----
@@ -375,7 +380,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     double acc = 0.0;
     {
       constexpr int D2 = 8;
-      int64_t wb = b & ~(int64_t)3;
+      int64_t wb = (dbg & 1) ? e : (b & ~(int64_t)3);
       for (; wb < e; wb += 128 * D2) {
         float4 t[D2];
 #pragma unroll
@@ -498,7 +503,9 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)cfg.dynamicSmemBytes);
     if (e != cudaSuccess) return e;
-    return cudaLaunchKernelEx(&cfg, kern, a, ws);
+    static int dbg = -1;
+    if (dbg < 0) dbg = getenv("HPAR_SEG_DEBUG") ? atoi(getenv("HPAR_SEG_DEBUG")) : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a, ws, dbg);
   };
   const bool f32 = a.out_dtype == DT_F32;
   if (a.verify) return f32 ? pick(segmented_kernel<true, true>) : pick(segmented_kernel<true, false>);

@@ -77,7 +77,7 @@ def c3_nest(with_gpu: bool = True, rows_chunk: int = 64, width: int = 8) -> list
     return lv
 
 
-def c3_fast_nest(with_gpu: bool = True, rows_chunk: int = 128) -> list[Level]:
+def c3_fast_nest(with_gpu: bool = True, rows_chunk: int = 256) -> list[Level]:
     """Config 3 (the fused CSR kernel's nest): rows (loop 0) dynamic(rows_chunk)
     over ALL warps of the GPU (cluster..warp collapsed: flags = intersection,
     dynamic and atomic hold); the block's nonzeros (loop 2 = the collapsed

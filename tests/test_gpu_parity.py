@@ -365,8 +365,9 @@ def test_segmented_csr_kernel(H, torch_mod, oracle, case):
         assert (count.cpu().numpy()[:nnz] == 1).all()
         own = owner.cpu().numpy()[:nnz] // 32  # warp of the owner
         lens = np.diff(off)
-        for b0 in range(0, rows, 128):
-            rs = [r for r in range(b0, min(b0 + 128, rows)) if 0 < lens[r] <= 1024]
+        rb = nests.c3_fast_nest()[1].chunk
+        for b0 in range(0, rows, rb):
+            rs = [r for r in range(b0, min(b0 + rb, rows)) if 0 < lens[r] <= 1024]
             if rs:
                 ws_ = np.concatenate([own[off[r]:off[r + 1]] for r in rs])
                 assert (ws_ == ws_[0]).all(), "a block's short rows span several warps"
