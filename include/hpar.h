@@ -212,7 +212,15 @@ hpar_status hpar_nest_info(hpar_nest_t nest, hpar_nest_info_t* out);
 hpar_status hpar_shard_range(hpar_nest_t nest, int64_t n0, int32_t rank, int64_t* begin, int64_t* count);
 
 /* ---- the hot path ---------------------------------------------------- */
-typedef enum { HPAR_OP_SUM = 0, HPAR_OP_MIN = 1, HPAR_OP_MAX = 2, HPAR_OP_HIST256 = 3 } hpar_op;
+/* HPAR_OP_AFFINE: an ordered, non-commutative user-defined operator (
+ * S:377).  int64 element x is the affine map y -> a*y + b (mod 2^64)
+ * with a = 2x+1, b = x*x; the fold composes the maps in ascending iteration
+ * order (left operand applied first), i.e. it runs the linear recurrence
+ * y <- a_i*y + b_i.  Result: uint64[2] = (A, B) of the composed map (per
+ * row when keyed; out_dtype HPAR_U64).  Node level: the per-rank maps are
+ * gathered and folded in rank order (never an NCCL reduction).  Served by
+ * the generic kernel (all trees are order-preserving). */
+typedef enum { HPAR_OP_SUM = 0, HPAR_OP_MIN = 1, HPAR_OP_MAX = 2, HPAR_OP_HIST256 = 3, HPAR_OP_AFFINE = 4 } hpar_op;
 typedef enum { HPAR_I32 = 0, HPAR_I64 = 1, HPAR_F32 = 2, HPAR_F64 = 3, HPAR_U8 = 4, HPAR_U64 = 5 } hpar_dtype;
 
 enum { HPAR_VERIFY_COVERAGE = 1, HPAR_VERIFY_PARTIALS = 2, HPAR_VERIFY_FINGERPRINT = 4 };

@@ -34,7 +34,11 @@
 /* ---- schedule codes (the oracle's own numbering) ------------------------ */
 enum { OR_STATIC = 0, OR_STATIC_CHUNK = 1, OR_DYNAMIC = 2, OR_NONE = 3 };
 /* ---- ops ---------------------------------------------------------------- */
-enum { OR_SUM = 0, OR_MIN = 1, OR_MAX = 2, OR_HIST256 = 3 };
+/* OR_AFFINE: element x (int64) is the affine map y -> a*y + b (mod 2^64)
+ * with a = 2x + 1, b = x*x (b = x would be conjugate to a product); the fold composes the maps in ascending order
+ * (apply the left operand first): associative, NOT commutative — the
+ * user-defined non-commutative reduction of P:86 / S:377. */
+enum { OR_SUM = 0, OR_MIN = 1, OR_MAX = 2, OR_HIST256 = 3, OR_AFFINE = 4 };
 /* ---- element types ------------------------------------------------------ */
 enum { OR_I32 = 0, OR_I64 = 1, OR_F32 = 2, OR_F64 = 3, OR_U8 = 4 };
 /* ---- error codes -------------------------------------------------------- */
@@ -135,6 +139,7 @@ typedef struct {
 typedef struct {
   int64_t i;
   double f;
+  uint64_t aa, ab;  /* OR_AFFINE: the map y -> aa*y + ab */
   uint64_t bins[256];
 } or_acc;
 
@@ -146,10 +151,19 @@ static void acc_identity(const or_walk* w, or_acc* a) {
   if (w->op == OR_MIN) { a->i = INT64_MAX; a->f = 1.0 / 0.0; }
   if (w->op == OR_MAX) { a->i = INT64_MIN; a->f = -1.0 / 0.0; }
   if (w->op == OR_HIST256) memset(a->bins, 0, sizeof(a->bins));
+  a->aa = 1;  /* identity map */
+  a->ab = 0;
 }
 
 /* fold b into a (a := a (+) b); ordered: a is the left operand */
 static void acc_fold(const or_walk* w, or_acc* a, const or_acc* b) {
+  if (w->op == OR_AFFINE) {  /* a := b o a  (a applied first) */
+    const uint64_t na = b->aa * a->aa;
+    const uint64_t nb = b->aa * a->ab + b->ab;
+    a->aa = na;
+    a->ab = nb;
+    return;
+  }
   if (w->op == OR_HIST256) {
     for (int k = 0; k < 256; ++k) a->bins[k] += b->bins[k];
     return;
@@ -173,6 +187,13 @@ static void acc_element(const or_walk* w, or_acc* a, int64_t idx) {
     a->bins[v] += 1;
     return;
   }
+  if (w->op == OR_AFFINE) {
+    const uint64_t v = (uint64_t)((const int64_t*)w->x)[idx];
+    e.aa = 2 * v + 1;
+    e.ab = v * v;
+    acc_fold(w, a, &e);
+    return;
+  }
   switch (w->dtype) {
     case OR_I32: e.i = ((const int32_t*)w->x)[idx]; break;
     case OR_I64: e.i = ((const int64_t*)w->x)[idx]; break;
@@ -184,7 +205,10 @@ static void acc_element(const or_walk* w, or_acc* a, int64_t idx) {
 }
 
 static void acc_store(const or_walk* w, void* arr, int64_t slot, const or_acc* a) {
-  if (w->op == OR_HIST256) {
+  if (w->op == OR_AFFINE) {
+    ((uint64_t*)arr)[2 * slot] = a->aa;
+    ((uint64_t*)arr)[2 * slot + 1] = a->ab;
+  } else if (w->op == OR_HIST256) {
     memcpy((uint64_t*)arr + slot * 256, a->bins, sizeof(a->bins));
   } else if (is_float(w->dtype)) {
     ((double*)arr)[slot] = a->f;
@@ -531,4 +555,15 @@ uint64_t or_fp_owner(const int64_t* owner, uint64_t begin, int64_t n) {
   uint64_t s = 0;
   for (int64_t e = 0; e < n; ++e) s += or_fp_mix2(begin + (uint64_t)e, (uint64_t)owner[e]);
   return s;
+}
+
+/* The recurrence the affine fold computes, run directly: y <- a_i*y + b_i for
+ * i ascending, from y0 (a different algorithm than composing maps). */
+uint64_t or_affine_run(const int64_t* x, int64_t n, uint64_t y0) {
+  uint64_t y = y0;
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t v = (uint64_t)x[i];
+    y = (2 * v + 1) * y + v * v;
+  }
+  return y;
 }

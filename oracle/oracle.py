@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(HERE, "liboracle.so")
 SRC_PATH = os.path.join(HERE, "oracle.c")
 
 STATIC, STATIC_CHUNK, DYNAMIC, NONE = 0, 1, 2, 3
-SUM, MIN, MAX, HIST256 = 0, 1, 2, 3
+SUM, MIN, MAX, HIST256, AFFINE = 0, 1, 2, 3, 4
 I32, I64, F32, F64, U8 = 0, 1, 2, 3, 4
 OK, E_SCHEDULE, E_INVALID, E_NOMEM = 0, -1, -2, -3
 
@@ -81,6 +81,8 @@ def lib():
                                     ctypes.c_void_p]
         L.or_segsum_f32.restype = None
         L.or_segsum_f32.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.or_affine_run.restype = ctypes.c_uint64
+        L.or_affine_run.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64]
         L.or_fp_mix.restype = ctypes.c_uint64
         L.or_fp_mix.argtypes = [ctypes.c_uint64]
         L.or_fp_mix2.restype = ctypes.c_uint64
@@ -167,22 +169,23 @@ def nest_run(levels: list[Level], *, n0: int, n1: int = 0, offsets: np.ndarray |
                 size = tasks
             if op == HIST256:
                 part_arrays[a] = np.zeros((size, 256), dtype=np.uint64)
+            elif op == AFFINE:
+                part_arrays[a] = np.zeros((size, 2), dtype=np.uint64)
             else:
                 part_arrays[a] = np.zeros(size, dtype=_ACC_NP[dt])
             part_ptrs[a] = part_arrays[a].ctypes.data
+    width = 256 if op == HIST256 else (2 if op == AFFINE else 0)
     if keyed:
-        result = np.zeros((n0, 256) if op == HIST256 else n0,
-                          dtype=np.uint64 if op == HIST256 else _ACC_NP[dt])
+        result = np.zeros((n0, width) if width else n0, dtype=np.uint64 if width else _ACC_NP[dt])
     else:
-        result = np.zeros(256 if op == HIST256 else 1,
-                          dtype=np.uint64 if op == HIST256 else _ACC_NP[dt])
+        result = np.zeros(width if width else 1, dtype=np.uint64 if width else _ACC_NP[dt])
     rc = lib().or_nest_run(ctypes.cast(arr, ctypes.c_void_p), nlev, nloops, n0, n1,
                            _ptr(offsets), dt, _ptr(x), ld if ld else n1, op, 1 if keyed else 0,
                            _ptr(result) if x is not None else None, _ptr(owner), _ptr(count),
                            ctypes.cast(part_ptrs, ctypes.c_void_p))
     if rc != 0:
         raise OracleError(rc, "nest_run")
-    if not keyed and op != HIST256:
+    if not keyed and op not in (HIST256, AFFINE):
         result = result[0]
     return NestResult(result if x is not None else None, owner, count, part_arrays)
 
@@ -263,3 +266,8 @@ def fp_once(begin: int, n: int) -> int:
 def fp_owner(owner: np.ndarray, begin: int) -> int:
     owner = np.ascontiguousarray(owner, dtype=np.int64)
     return int(lib().or_fp_owner(_ptr(owner), begin, owner.size))
+
+
+def affine_run(x: np.ndarray, y0: int = 0) -> int:
+    x = np.ascontiguousarray(x, dtype=np.int64)
+    return int(lib().or_affine_run(_ptr(x), x.size, y0))

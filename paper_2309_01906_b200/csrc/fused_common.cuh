@@ -71,9 +71,7 @@ __device__ void fused_total_climb(const NestArgs& a, Acc v, int W, ClimbSmem<Acc
       for (int w = 0; w < W; ++w) r = OpT<OP, Acc>::combine(r, sh.warp[w]);
       v = r;
       export_slot<Acc>(a, S_CTA, (int64_t)blockIdx.x, v);
-      union { Acc x; unsigned long long u; } cv;
-      cv.x = v;
-      st_cluster_u64(mapa(smem_addr(&sh.cta[rank]), 0), cv.u);
+      st_cluster_acc(mapa(smem_addr(&sh.cta[rank]), 0), v);
     }
   }
   cluster_sync_all();

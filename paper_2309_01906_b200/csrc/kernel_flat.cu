@@ -179,7 +179,7 @@ cudaError_t launch_v(const NestArgs& a, int W, int tile, cudaStream_t s) {
 // Does the nest have the coalesced flat shape (and the call suit the kernel)?
 bool flat_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 1 || a.keyed) { *why = "not a flat total"; return false; }
-  if (a.op == OP_HIST) { *why = "hist"; return false; }
+  if (a.op == OP_HIST || a.op == OP_AFFINE) { *why = "sum/min/max only"; return false; }
   if (a.in_dtype != DT_F32 && a.in_dtype != DT_I32) { *why = "dtype"; return false; }
   if (((uintptr_t)a.in & 15) != 0) { *why = "input not 16-byte aligned"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }

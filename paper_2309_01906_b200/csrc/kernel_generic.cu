@@ -17,6 +17,7 @@
 // shape; this one trades speed for generality.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 #include "level_primitives.cuh"
 #include "plan.h"
 
@@ -133,9 +134,9 @@ struct Generic {
 
   __device__ __forceinline__ Acc load(int64_t i, int64_t j) const {
     const In* x = (const In*)a.in;
-    if (a.nloops == 1) return (Acc)x[i];
-    if (a.offsets) return (Acc)x[a.offsets[i] + j];
-    return (Acc)x[i * a.ld + j];
+    if (a.nloops == 1) return ElemT<OP, Acc, In>::make(x[i]);
+    if (a.offsets) return ElemT<OP, Acc, In>::make(x[a.offsets[i] + j]);
+    return ElemT<OP, Acc, In>::make(x[i * a.ld + j]);
   }
   __device__ __forceinline__ int64_t iter_index(int64_t i, int64_t j) const {
     if (a.nloops == 1) return i;
@@ -202,7 +203,7 @@ struct Generic {
       const unsigned grp = (a.lane_w == 32) ? 0xffffffffu
                                              : (((1u << a.lane_w) - 1u) << ((lane / a.lane_w) * a.lane_w));
       for (int off = 1; off < a.lane_w; off <<= 1) {
-        Acc o = __shfl_down_sync(grp, v, off, a.lane_w);
+        Acc o = shfl_down_t(grp, v, off, a.lane_w);
         if (((lane % a.lane_w) & (2 * off - 1)) == 0) v = OpT<OP, Acc>::combine(v, o);
       }
     }
@@ -225,11 +226,7 @@ struct Generic {
     }
     // step CTA -> CLUSTER (DSMEM slots in the leader CTA + cluster barrier)
     if (stop < S_CTA) {
-      if (threadIdx.x == 0) {
-        union { Acc x; unsigned long long u; } cv;
-        cv.x = v;
-        st_cluster_u64(mapa(smem_addr(&sh.cta[parity][cta_rank]), 0), cv.u);
-      }
+      if (threadIdx.x == 0) st_cluster_acc(mapa(smem_addr(&sh.cta[parity][cta_rank]), 0), v);
       cluster_sync_all();
       if (cta_rank == 0 && threadIdx.x == 0) {
         Acc r = OpT<OP, Acc>::identity();
@@ -243,8 +240,13 @@ struct Generic {
   }
 
   __device__ void write_row(int64_t i, Acc v) const {
-    if (a.out_dtype == DT_F32) ((float*)a.out)[i] = (float)v;
-    else ((Acc*)a.out)[i] = v;
+    if constexpr (std::is_arithmetic<Acc>::value) {
+      if (a.out_dtype == DT_F32) {
+        ((float*)a.out)[i] = (float)v;
+        return;
+      }
+    }
+    ((Acc*)a.out)[i] = v;
   }
 
   __device__ void run() {
@@ -305,7 +307,11 @@ struct Generic {
     }
 
     if (!keyed) acc = climb(acc, S_GPU, -1);
-    // grid level: single-pass ticket (cluster -> GPU), also resets the tickets
+    // grid level: single-pass ticket (cluster -> GPU), also resets the tickets.
+    // The leader arrives for its whole cluster, so every CTA of the cluster
+    // must be done (no more claims) first: in keyed mode no climb has synced
+    // the cluster yet.
+    if (keyed) cluster_sync_all();
     __syncthreads();
     const bool leader_cta = (cta_rank == 0);
     if (leader_cta) {
@@ -369,7 +375,22 @@ cudaError_t launch_generic(const NestArgs& a, int threads, cudaStream_t s) {
   if (dt == DT_F32) { HPAR_G(float, double) }
   if (dt == DT_F64) { HPAR_G(double, double) }
 #undef HPAR_G
+  if (op == OP_AFFINE && dt == DT_I64) return launch_t<long long, Aff, OP_AFFINE>(a, threads, s);
   return cudaErrorInvalidValue;
+}
+
+// node level of an ordered op: fold the G per-rank results (gathered by
+// ncclAllGather in rank order) in ascending rank order
+__global__ void affine_rank_fold_kernel(const Aff* in, int G, Aff* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    Aff v = OpT<OP_AFFINE, Aff>::identity();
+    for (int g = 0; g < G; ++g) v = OpT<OP_AFFINE, Aff>::combine(v, in[g]);
+    *out = v;
+  }
+}
+cudaError_t launch_affine_rank_fold(const void* gathered, int G, void* out, cudaStream_t s) {
+  affine_rank_fold_kernel<<<1, 32, 0, s>>>((const Aff*)gathered, G, (Aff*)out);
+  return cudaGetLastError();
 }
 
 }  // namespace hpar

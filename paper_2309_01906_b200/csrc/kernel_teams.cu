@@ -85,7 +85,7 @@ cudaError_t launch_t(const NestArgs& a, int W, int chunk, cudaStream_t s) {
 
 bool teams_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 2 || a.keyed || a.offsets) { *why = "not a dense 2-loop total"; return false; }
-  if (a.op == OP_HIST) { *why = "hist"; return false; }
+  if (a.op == OP_HIST || a.op == OP_AFFINE) { *why = "sum/min/max only"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
   LevelView v = device_levels(a);
   if (v.n != 2) { *why = "needs teams and threads levels"; return false; }

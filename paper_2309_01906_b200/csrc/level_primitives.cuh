@@ -48,6 +48,50 @@ struct OpT<OP_MAX, long long> {
   __device__ __forceinline__ static long long combine(long long a, long long b) { return b > a ? b : a; }
 };
 
+// Ordered user-defined operator: element x is the affine map
+// y -> a*y + b (mod 2^64) with a = 2x+1, b = x*x; combine(L, R) applies L then
+// R.  Associative, not commutative: only order-preserving trees are correct.
+struct Aff {
+  unsigned long long a, b;
+};
+template <>
+struct OpT<OP_AFFINE, Aff> {
+  __device__ __forceinline__ static Aff identity() { return Aff{1ull, 0ull}; }
+  __device__ __forceinline__ static Aff combine(Aff l, Aff r) { return Aff{r.a * l.a, r.a * l.b + r.b}; }
+};
+// input element -> accumulator
+template <int OP, typename Acc, typename In>
+struct ElemT {
+  __device__ __forceinline__ static Acc make(In x) { return (Acc)x; }
+};
+template <typename In>
+struct ElemT<OP_AFFINE, Aff, In> {
+  __device__ __forceinline__ static Aff make(In x) {
+    const unsigned long long v = (unsigned long long)x;
+    return Aff{2ull * v + 1ull, v * v};
+  }
+};
+
+// shuffles that also move the 16-byte ordered accumulator
+template <typename T>
+__device__ __forceinline__ T shfl_down_t(unsigned mask, T v, int off, int width = 32) {
+  return __shfl_down_sync(mask, v, off, width);
+}
+template <>
+__device__ __forceinline__ Aff shfl_down_t<Aff>(unsigned mask, Aff v, int off, int width) {
+  return Aff{__shfl_down_sync(mask, v.a, off, width), __shfl_down_sync(mask, v.b, off, width)};
+}
+// L2-coherent read of a value another CTA published (after a fence + ticket)
+template <typename T>
+__device__ __forceinline__ T ld_volatile(const T* p) {
+  return *(const volatile T*)p;
+}
+template <>
+__device__ __forceinline__ Aff ld_volatile<Aff>(const Aff* p) {
+  const volatile unsigned long long* q = (const volatile unsigned long long*)p;
+  return Aff{q[0], q[1]};
+}
+
 // --------------------------------------------------- lane level: shuffle ----
 // Order-preserving tree over `count` consecutive groups of `stride` lanes:
 // after the call the first lane of every block of stride*count lanes holds
@@ -57,7 +101,7 @@ template <int OP, typename Acc>
 __device__ __forceinline__ Acc shfl_tree(Acc v, int stride, int count) {
   const int lane = threadIdx.x & 31;
   for (int off = stride; off < stride * count; off <<= 1) {
-    Acc other = __shfl_down_sync(0xffffffffu, v, off);
+    Acc other = shfl_down_t(0xffffffffu, v, off);
     if ((lane & (2 * off - 1)) == 0) v = OpT<OP, Acc>::combine(v, other);
   }
   return v;
@@ -68,7 +112,7 @@ template <int OP, typename Acc>
 __device__ __forceinline__ Acc warp_fold(Acc v) {
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    Acc other = __shfl_down_sync(0xffffffffu, v, off);
+    Acc other = shfl_down_t(0xffffffffu, v, off);
     if ((threadIdx.x & (2 * off - 1)) == 0) v = OpT<OP, Acc>::combine(v, other);
   }
   return v;
@@ -96,6 +140,14 @@ __device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
 }
 __device__ __forceinline__ void st_cluster_u64(uint32_t addr, unsigned long long v) {
   asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+// store an accumulator (8 or 16 bytes) to a shared::cluster address
+template <typename Acc>
+__device__ __forceinline__ void st_cluster_acc(uint32_t addr, const Acc& v) {
+  static_assert(sizeof(Acc) % 8 == 0, "accumulators are whole 8-byte words");
+  const unsigned long long* w = (const unsigned long long*)&v;
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Acc) / 8); ++i) st_cluster_u64(addr + 8 * i, w[i]);
 }
 __device__ __forceinline__ unsigned long long ld_cluster_u64(uint32_t addr) {
   unsigned long long v;
@@ -263,13 +315,13 @@ __device__ __forceinline__ bool grid_arrive(Acc my, Acc* partials, unsigned int*
 // contiguous block, then an ordered tree over the threads.  Result returned
 // in thread 0.  `s_warp` holds >= 32 accumulators of shared memory.
 template <int OP, typename Acc>
-__device__ Acc block_fold_ordered(const volatile Acc* partials, int64_t C, Acc* s_warp) {
+__device__ Acc block_fold_ordered(const Acc* partials, int64_t C, Acc* s_warp) {
   const int nthr = blockDim.x;
   const int64_t per = (C + nthr - 1) / nthr;
   const int64_t b = (int64_t)threadIdx.x * per;
   const int64_t e = (b + per < C) ? b + per : C;
   Acc v = OpT<OP, Acc>::identity();
-  for (int64_t i = b; i < e; ++i) v = OpT<OP, Acc>::combine(v, partials[i]);
+  for (int64_t i = b; i < e; ++i) v = OpT<OP, Acc>::combine(v, ld_volatile(partials + i));
   v = warp_fold<OP>(v);
   const int w = threadIdx.x >> 5, nw = nthr >> 5;
   if ((threadIdx.x & 31) == 0) s_warp[w] = v;

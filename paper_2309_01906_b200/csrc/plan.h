@@ -14,7 +14,7 @@ enum Slot { S_GPU = 0, S_CLUSTER = 1, S_CTA = 2, S_WARP = 3, S_LANE = 4, S_LANE_
 constexpr int kMaxLev = 8;
 
 enum Sched { SCHED_STATIC = 0, SCHED_STATIC_CHUNK = 1, SCHED_DYNAMIC = 2, SCHED_NONE = 3 };
-enum Op { OP_SUM = 0, OP_MIN = 1, OP_MAX = 2, OP_HIST = 3 };
+enum Op { OP_SUM = 0, OP_MIN = 1, OP_MAX = 2, OP_HIST = 3, OP_AFFINE = 4 };
 enum DType { DT_I32 = 0, DT_I64 = 1, DT_F32 = 2, DT_F64 = 3, DT_U8 = 4, DT_U64 = 5 };
 enum Verify { V_COVERAGE = 1, V_PARTIALS = 2, V_FINGERPRINT = 4 };
 

@@ -37,6 +37,7 @@ bool segmented_matches(const NestArgs& a, const char** why);
 cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaStream_t s, const char** name);
 size_t segmented_ws_bytes(int64_t nnz);
 void segmented_ws_qrow(int64_t nnz, size_t* off, size_t* len);
+cudaError_t launch_affine_rank_fold(const void* gathered, int G, void* out, cudaStream_t s);
 bool teams_matches(const NestArgs& a, const char** why);
 cudaError_t launch_teams(const NestArgs& a, int W, cudaStream_t s, const char** name);
 }  // namespace hpar
@@ -75,6 +76,7 @@ struct NcclApi {
   std::string why;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
       nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commCount)(const ncclComm_t, int*) = nullptr;
   ncclResult_t (*commUserRank)(const ncclComm_t, int*) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
@@ -93,6 +95,7 @@ void load_nccl() {
     return;
   }
   g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
   g_nccl.commCount = (decltype(g_nccl.commCount))dlsym(h, "ncclCommCount");
   g_nccl.commUserRank = (decltype(g_nccl.commUserRank))dlsym(h, "ncclCommUserRank");
   g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
@@ -253,6 +256,7 @@ struct hpar_nest {
   int32_t* error_flag = nullptr;
   int* barrier_word = nullptr;
   std::string last_kernel = "none";
+  void* gather_buf = nullptr;  // node level of ordered ops: G gathered results
   void* seg_ws = nullptr;  // CSR segmented kernel workspace (grown on demand)
   size_t seg_ws_bytes = 0;
 };
@@ -486,6 +490,7 @@ extern "C" hpar_status hpar_nest_destroy(hpar_nest_t n) {
     cudaFree(n->error_flag);
     cudaFree(n->barrier_word);
     cudaFree(n->seg_ws);
+    cudaFree(n->gather_buf);
   }
   delete n;
   return ok();
@@ -575,8 +580,10 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   cudaStream_t stream = (cudaStream_t)stream_;
   // ---- op / dtype ----
   const bool hist = d->op == HPAR_OP_HIST256;
-  if (d->op < 0 || d->op > 3) return fail(HPAR_E_UNSUPPORTED, "unknown op %d", d->op);
+  const bool affine = d->op == HPAR_OP_AFFINE;
+  if (d->op < 0 || d->op > 4) return fail(HPAR_E_UNSUPPORTED, "unknown op %d", d->op);
   if (hist && d->in_dtype != HPAR_U8) return fail(HPAR_E_UNSUPPORTED, "hist256 needs uint8 input");
+  if (affine && d->in_dtype != HPAR_I64) return fail(HPAR_E_UNSUPPORTED, "affine needs int64 input");
   if (!hist && !(d->in_dtype == HPAR_I32 || d->in_dtype == HPAR_I64 || d->in_dtype == HPAR_F32 ||
                  d->in_dtype == HPAR_F64))
     return fail(HPAR_E_UNSUPPORTED, "op %d: input dtype %d not supported (i32/i64/f32/f64)", d->op, d->in_dtype);
@@ -696,7 +703,11 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
     const bool fin = d->in_dtype == HPAR_F32 || d->in_dtype == HPAR_F64;
     if (fin && d->out_dtype != HPAR_F32 && d->out_dtype != HPAR_F64)
       return fail(HPAR_E_INVALID, "keyed fp results: out_dtype must be f32 or f64");
-    if (!fin && d->out_dtype != HPAR_I64) return fail(HPAR_E_INVALID, "keyed int results: out_dtype must be i64");
+    if (affine) {
+      if (d->out_dtype != HPAR_U64) return fail(HPAR_E_INVALID, "keyed affine results: out_dtype must be u64 (2 per row)");
+    } else if (!fin && d->out_dtype != HPAR_I64) {
+      return fail(HPAR_E_INVALID, "keyed int results: out_dtype must be i64");
+    }
     A.out_dtype = d->out_dtype;
   } else {
     A.out_dtype = (d->in_dtype == HPAR_F32 || d->in_dtype == HPAR_F64) ? HPAR_F64 : HPAR_I64;
@@ -759,7 +770,21 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   n->last_kernel = name;
 
   // ---- node level: one allreduce over NVLink (§8(a) A9) ----
-  if (!d->keyed && n->nranks > 1) {
+  if (!d->keyed && n->nranks > 1 && affine) {
+    // an ordered op cannot be an NCCL reduction: gather the per-rank results
+    // in rank order (= the GPU level's static-block order) and fold them
+    hpar_status s = need_nccl();
+    if (s) return s;
+    if (!g_nccl.allGather) return fail(HPAR_E_NCCL, "ncclAllGather unavailable");
+    if (!n->gather_buf) {
+      cudaError_t ae = cudaMalloc(&n->gather_buf, (size_t)n->nranks * 16);
+      if (ae != cudaSuccess) return fail(HPAR_E_NOMEM, "gather buffer: %s", cudaGetErrorString(ae));
+    }
+    ncclResult_t r = g_nccl.allGather(d->out, n->gather_buf, 2, ncclUint64, (ncclComm_t)n->comm, stream);
+    if (r != ncclSuccess) return nccl_fail(r, (ncclComm_t)n->comm, "ncclAllGather");
+    e = launch_affine_rank_fold(n->gather_buf, n->nranks, d->out, stream);
+    if (e != cudaSuccess) return fail(HPAR_E_CUDA, "rank fold: %s", cudaGetErrorString(e));
+  } else if (!d->keyed && n->nranks > 1) {
     hpar_status s = need_nccl();
     if (s) return s;
     ncclDataType_t t;

@@ -29,7 +29,7 @@ PROPS = ["barrier", "critical", "atomic", "shuffle", "oversubscribable", "dynami
          "progress", "globalmem", "localmem", "groupmem", "cache"]
 P = {name: 1 << i for i, name in enumerate(PROPS)}
 STATIC, STATIC_CHUNK, DYNAMIC, NONE = 0, 1, 2, 3
-OP_SUM, OP_MIN, OP_MAX, OP_HIST256 = 0, 1, 2, 3
+OP_SUM, OP_MIN, OP_MAX, OP_HIST256, OP_AFFINE = 0, 1, 2, 3, 4
 I32, I64, F32, F64, U8, U64 = 0, 1, 2, 3, 4, 5
 VERIFY_COVERAGE, VERIFY_PARTIALS, VERIFY_FINGERPRINT = 1, 2, 4
 MAX_NEST = 8

@@ -70,7 +70,9 @@ def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, 
         n_iter = n0 * (n1 if nloops == 2 else 1)
     xd = torch.from_numpy(x).cuda()
     fp = x.dtype.kind == "f"
-    if keyed:
+    if op == H.OP_AFFINE:
+        out = torch.zeros((n0, 2) if keyed else (2,), dtype=torch.int64, device="cuda")
+    elif keyed:
         out = torch.zeros(n0, dtype=torch.float64 if fp else torch.int64, device="cuda")
     elif op == H.OP_HIST256:
         out = torch.zeros(256, dtype=torch.int64, device="cuda")
@@ -96,14 +98,14 @@ def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, 
             else:
                 tot *= T
                 size = tot
-            shape = (size, 256) if op == H.OP_HIST256 else (size,)
+            shape = (size, 256) if op == H.OP_HIST256 else ((size, 2) if op == H.OP_AFFINE else (size,))
             parts.append(torch.full(shape, -7, dtype=torch.float64 if (fp and op != H.OP_HIST256) else torch.int64,
                                     device="cuda"))
     offs = torch.from_numpy(offsets).cuda() if offsets is not None else None
     verify = (H.VERIFY_COVERAGE if coverage else 0) | (H.VERIFY_PARTIALS if partials else 0)
     d = H.make_desc(xd, out, op=op, n0=n0, n1=n1, ld=n1, nloops=nloops, keyed=keyed, offsets=offs,
                     max_inner=max_inner, verify=verify, partials=parts, owner=owner, count=count,
-                    out_dtype=(H.F64 if fp else H.I64) if keyed else -1)
+                    out_dtype=(H.U64 if op == H.OP_AFFINE else (H.F64 if fp else H.I64)) if keyed else -1)
     nest.parallel_for_reduce(d)
     torch.cuda.synchronize()
     res = out.cpu().numpy()
@@ -119,8 +121,8 @@ def compare(oracle, H, levels, res, x, *, n0, n1=0, offsets=None, keyed=False, o
                         nloops=2 if (n1 or offsets is not None) else 1)
     fp = x.dtype.kind == "f"
     # result
-    if op == H.OP_HIST256:
-        assert np.array_equal(res["out"].astype(np.uint64), o.result)
+    if op in (H.OP_HIST256, H.OP_AFFINE):
+        assert np.array_equal(res["out"].view(np.uint64), o.result)
     elif fp:
         assert_rel(res["out"] if keyed else res["out"][0], o.result)
     else:
@@ -135,10 +137,10 @@ def compare(oracle, H, levels, res, x, *, n0, n1=0, offsets=None, keyed=False, o
         for a, p in enumerate(res["parts"]):
             if p is None or o.partials[a] is None:
                 continue
-            if op == H.OP_HIST256:
+            if op in (H.OP_HIST256, H.OP_AFFINE):
                 if np.all(p == -7):
                     continue  # level without materialised bins (lanes)
-                assert np.array_equal(p.astype(np.uint64), o.partials[a]), f"level {a} partials"
+                assert np.array_equal(p.view(np.uint64), o.partials[a]), f"level {a} partials"
             elif fp:
                 assert_rel(p, o.partials[a])
             else:
@@ -398,3 +400,65 @@ def test_hierarchy_query_matches_device(H, torch_mod):
     assert t[H.HPAR_GPU].groupmem_bytes == p.total_memory
     assert t[H.HPAR_CLUSTER].num >= p.multi_processor_count // 2
     assert "barrier" not in t[H.HPAR_CLUSTER].flags() and "shuffle" in t[H.HPAR_LANE].flags()
+
+
+def test_ordered_affine_op(H, torch_mod, oracle):
+    """NEXT f2: a non-commutative user-defined operator
+    (affine-map composition mod 2^64) through the generic kernel.  Every GPU
+    tree is order-preserving, so results and per-level partials equal the
+    oracle's ascending-task-order fold BIT FOR BIT for any static nest; with
+    block schedules that is the sequential recurrence itself."""
+    torch = torch_mod
+    rng = random.Random(86)
+    done = 0
+    while done < 25:
+        levels = random_flat_nest(H, rng, 0)
+        for l in levels:
+            if l.schedule == H.NONE:
+                l.schedule = H.STATIC
+        C, K, W = rng.choice([1, 3, 5]), rng.choice([1, 2, 4]), rng.choice([1, 2, 4])
+        n = rng.randint(0, 6000)
+        x = gen.gen_i32(done + 300, 0, n).astype(np.int64)
+        res = run_nest(H, torch, levels, x, n0=n, op=H.OP_AFFINE, C=C, K=K, W=W)
+        assert res["kernel"] == "generic"
+        compare(oracle, H, levels, res, x, n0=n, op=H.OP_AFFINE, C=C, K=K, W=W)
+        done += 1
+    # block schedules everywhere: the fold is the sequential recurrence
+    levels = [H.Level(H.HPAR_GPU), H.Level(H.HPAR_CLUSTER), H.Level(H.HPAR_CTA), H.Level(H.HPAR_WARP),
+              H.Level(H.HPAR_LANE)]
+    x = gen.gen_i32(4242, 0, 100003).astype(np.int64)
+    res = run_nest(H, torch, levels, x, n0=x.size, op=H.OP_AFFINE, C=7, K=2, W=4, coverage=False, partials=False)
+    A, B = (int(v) for v in res["out"].view(np.uint64))
+    assert (A * 5 + B) % (1 << 64) == oracle.affine_run(x, 5)
+    # keyed rows (2 loops): per-row composed maps
+    levels = [H.Level(H.HPAR_GPU, H.HPAR_GPU, 0, loop=0), H.Level(H.HPAR_CLUSTER, H.HPAR_CTA, 0, loop=0),
+              H.Level(H.HPAR_WARP, H.HPAR_LANE, 1, loop=1, chunk=2)]
+    x = gen.gen_i32(77, 0, 29 * 333).astype(np.int64)
+    res = run_nest(H, torch, levels, x, n0=29, n1=333, keyed=True, op=H.OP_AFFINE, C=3, K=2, W=2)
+    compare(oracle, H, levels, res, x, n0=29, n1=333, keyed=True, op=H.OP_AFFINE, C=3, K=2, W=2)
+
+
+def test_generic_keyed_dynamic_repeated_calls(H, torch_mod, oracle):
+    """Regression: in keyed mode every CTA of a cluster must be done before the
+    cluster's leader arrives at the grid ticket (whose last arriver resets the
+    dynamic tickets).  Same nest, several calls, K = 2 and 4."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    off = gen.csr_offsets(3000, 40000)
+    v = gen.gen_f32(gen.SEED_C3, 0, 40000)
+    want = oracle.segsum_f32(v, off)
+    for K in (2, 4):
+        nest = H.Nest(nests.c3_nest(with_gpu=True, rows_chunk=64, width=8), device=0, cluster_dim=K,
+                      warps_per_cta=4, clusters=3)
+        xd = torch.from_numpy(v).cuda()
+        offd = torch.from_numpy(off).cuda()
+        for _ in range(4):
+            out = torch.zeros(3000, dtype=torch.float64, device="cuda")
+            owner = torch.zeros(40000, dtype=torch.int64, device="cuda")
+            count = torch.zeros(40000, dtype=torch.int32, device="cuda")
+            nest.parallel_for_reduce(H.make_desc(xd, out, n0=3000, nloops=2, keyed=True, offsets=offd,
+                                                 out_dtype=H.F64, verify=H.VERIFY_COVERAGE, owner=owner,
+                                                 count=count))
+            torch.cuda.synchronize()
+            assert (count.cpu().numpy() == 1).all()
+            assert_rel(out.cpu().numpy(), want)

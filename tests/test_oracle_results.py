@@ -159,3 +159,38 @@ def test_fingerprints(oracle):
     f = oracle.fp_owner(owner, b)
     owner[1234] += 1
     assert oracle.fp_owner(owner, b) != f
+
+
+def _compose(maps):
+    a, b = 1, 0
+    for ma, mb in maps:
+        a, b = (int(ma) * a) % (1 << 64), (int(ma) * b + int(mb)) % (1 << 64)
+    return a, b
+
+
+def test_affine_ordered_fold(oracle):
+    """NEXT f2: the ordered fold of a non-commutative
+    operator.  With block (static, no chunk) schedules at every level each
+    task owns a contiguous, in-order run, so the hierarchical fold in
+    ascending task order equals running the recurrence y <- (2x+1) y + x
+    directly; with round-robin schedules it is the S:377 task-order fold,
+    which differs.  Every parent is the ordered composition of its children."""
+    x = gen.gen_i32(17, 0, 5003).astype(np.int64)
+    block = [[(2, 0, 0, 0), (3, 0, 0, 0), (4, 0, 0, 0), (32, 0, 0, 0)], [(5, 0, 0, 0), (7, 0, 0, 0)]]
+    for lv in block:
+        levels = [oracle.Level(T=T, sched=s, chunk=c, loop=l) for (T, s, c, l) in lv]
+        r = oracle.nest_run(levels, n0=x.size, x=x, op=oracle.AFFINE)
+        A, B = int(r.result[0]), int(r.result[1])
+        for y0 in (0, 1, 987654321):
+            assert (A * y0 + B) % (1 << 64) == oracle.affine_run(x, y0)
+    for lv in NESTS:
+        levels = [oracle.Level(T=T, sched=s, chunk=c, loop=l) for (T, s, c, l) in lv]
+        r = oracle.nest_run(levels, n0=x.size, x=x, op=oracle.AFFINE)
+        res = (int(r.result[0]), int(r.result[1]))
+        assert _compose(r.partials[0]) == res
+        for a in range(1, len(lv)):
+            T = lv[a][0]
+            kids = r.partials[a].reshape(-1, T, 2)
+            for pidx in range(kids.shape[0]):
+                assert _compose(kids[pidx]) == tuple(int(v) for v in r.partials[a - 1][pidx])
+    assert oracle.affine_run(x[::-1].copy(), 3) != oracle.affine_run(x, 3)
