@@ -279,6 +279,36 @@ hpar_status hpar_parallel_for_reduce(hpar_nest_t nest, const hpar_reduce_desc* d
  * added to it (0 = barrier visibility holds).  HPAR_NODE: no-op. */
 hpar_status hpar_barrier(hpar_nest_t nest, int32_t level, uint64_t* probe_mismatches, void* stream);
 
+/* ---- property-based level selection (§3.2-3.3) --------------
+ * A construct `parallel sync(demand) reserve(sync(reserve))` asks for levels
+ * by the Table-2 properties it needs instead of naming them.  Constructs are
+ * given outermost first; each takes a contiguous run of the still-unassigned
+ * hardware levels starting at the first one (levels are never skipped), the
+ * LONGEST run whose collapsed flags (intersection) contain `demand`
+ * while the remaining levels can still serve the inner constructs (maximal
+ * fan-out: "would use all available parallelism"; SPEC policy S:283).
+ * `reserve` additionally requires the levels left to the inner constructs
+ * to satisfy it.  The innermost construct must end at the lane
+ * level.  Output: one hpar_nest_level per construct (first/last filled,
+ * schedule/loop/chunk copied), ready for hpar_nest_create.
+ * Errors: HPAR_E_CAPABILITY when no assignment satisfies the demands
+ * ("unsatisfiable sync demand"), HPAR_E_INVALID on bad arguments. */
+typedef struct {
+  uint32_t demand;   /* HPAR_P_* flags the construct needs (0 = sync())       */
+  uint32_t reserve;  /* flags the levels left to inner constructs must offer  */
+  int32_t schedule;  /* copied to the nest level                               */
+  int32_t loop;
+  int64_t chunk;
+} hpar_sync_construct;
+
+hpar_status hpar_nest_resolve(const hpar_sync_construct* constructs, int32_t n, const hpar_level_info* table,
+                              hpar_nest_level* out);
+
+/* Portable level aliases: "devices" = gpu, "teams" =
+ * cluster..cta, "threads" = warp..lane, "simd" = lane, plus the hardware
+ * level names.  Writes the hardware range of `name`. */
+hpar_status hpar_level_alias(const char* name, int32_t* first, int32_t* last);
+
 /* Thread-local text of the last error ("" if none). */
 const char* hpar_last_error(void);
 /* Name of the kernel specialisation the last hpar_parallel_for_reduce on

@@ -827,3 +827,83 @@ extern "C" hpar_status hpar_barrier(hpar_nest_t n, int32_t level, uint64_t* mism
   if (e != cudaSuccess) return fail(HPAR_E_CUDA, "barrier probe: %s", cudaGetErrorString(e));
   return ok();
 }
+
+// ------------------------------------------- property-based selection ----
+// §3.2-3.3; SPEC level_resolver with the selection
+// policy of S:283: each construct takes the longest feasible run of the
+// remaining levels, starting at the first one.
+namespace {
+uint32_t run_flags(const hpar_level_info* t, int first, int last) {
+  uint32_t f = 0xFFFFFFFFu;
+  for (int l = first; l <= last; ++l) f &= t[l].props;
+  return f;
+}
+// can constructs [k, n) be assigned to the levels [s, HPAR_LANE]?  fills ends[]
+bool assign(const hpar_sync_construct* c, int n, int k, int s, const hpar_level_info* t, int* ends) {
+  if (k == n) return s > HPAR_LANE;  // every level used, nothing left over
+  if (s > HPAR_LANE) return false;
+  // without a reserve: the longest run first (maximal fan-out);
+  // with a reserve: the shortest run first, i.e. the inner constructs get every
+  // level that matches the reserve ("uses all levels except the ones that
+  // match the reserve clause argument")
+  const bool res = c[k].reserve != 0;
+  for (int i = 0; i <= HPAR_LANE - s; ++i) {
+    const int e = res ? s + i : HPAR_LANE - i;
+    const uint32_t f = run_flags(t, s, e);
+    if ((f & c[k].demand) != c[k].demand) continue;
+    if (c[k].reserve && e < HPAR_LANE) {
+      const uint32_t rest = run_flags(t, e + 1, HPAR_LANE);
+      if ((rest & c[k].reserve) != c[k].reserve) continue;
+    } else if (c[k].reserve && e == HPAR_LANE) {
+      continue;  // a reserve needs levels left over
+    }
+    if (assign(c, n, k + 1, e + 1, t, ends)) {
+      ends[k] = e;
+      return true;
+    }
+  }
+  return false;
+}
+}  // namespace
+
+extern "C" hpar_status hpar_nest_resolve(const hpar_sync_construct* c, int32_t n, const hpar_level_info* table,
+                                         hpar_nest_level* out) {
+  if (!c || !table || !out || n < 1 || n > HPAR_MAX_NEST)
+    return fail(HPAR_E_INVALID, "hpar_nest_resolve: bad arguments");
+  // the outermost construct starts at the coarsest level from which the
+  // demands are satisfiable; levels above it run a single task
+  int ends[HPAR_MAX_NEST];
+  int s0 = HPAR_GPU;
+  while (s0 <= HPAR_LANE && !assign(c, n, 0, s0, table, ends)) ++s0;
+  if (s0 > HPAR_LANE)
+    return fail(HPAR_E_CAPABILITY,
+                "no assignment of the %d construct(s) to contiguous level runs satisfies their sync demands "
+                "(S:229 unsatisfiable sync demand)", n);
+  int s = s0;
+  for (int k = 0; k < n; ++k) {
+    memset(&out[k], 0, sizeof(out[k]));
+    out[k].first = s;
+    out[k].last = ends[k];
+    out[k].schedule = c[k].schedule;
+    out[k].loop = c[k].loop;
+    out[k].chunk = c[k].chunk;
+    s = ends[k] + 1;
+  }
+  return ok();
+}
+
+extern "C" hpar_status hpar_level_alias(const char* name, int32_t* first, int32_t* last) {
+  if (!name || !first || !last) return fail(HPAR_E_INVALID, "hpar_level_alias: NULL argument");
+  struct { const char* n; int f, l; } tab[] = {
+      {"devices", HPAR_GPU, HPAR_GPU},   {"gpu", HPAR_GPU, HPAR_GPU},         {"teams", HPAR_CLUSTER, HPAR_CTA},
+      {"cluster", HPAR_CLUSTER, HPAR_CLUSTER}, {"cta", HPAR_CTA, HPAR_CTA},   {"threads", HPAR_WARP, HPAR_LANE},
+      {"warp", HPAR_WARP, HPAR_WARP},    {"lane", HPAR_LANE, HPAR_LANE},      {"simd", HPAR_LANE, HPAR_LANE},
+      {"node", HPAR_NODE, HPAR_NODE}};
+  for (auto& e : tab)
+    if (strcmp(e.n, name) == 0) {
+      *first = e.f;
+      *last = e.l;
+      return ok();
+    }
+  return fail(HPAR_E_INVALID, "unknown level or alias '%s'", name);
+}

@@ -80,6 +80,11 @@ class NestConfig(ctypes.Structure):
                 ("clusters", ctypes.c_int64), ("nccl_comm", ctypes.c_void_p), ("desc", ctypes.POINTER(DeviceDesc))]
 
 
+class SyncConstruct(ctypes.Structure):
+    _fields_ = [("demand", ctypes.c_uint32), ("reserve", ctypes.c_uint32), ("schedule", ctypes.c_int32),
+                ("loop", ctypes.c_int32), ("chunk", ctypes.c_int64)]
+
+
 class NestInfo(ctypes.Structure):
     _fields_ = [("G", ctypes.c_int64), ("C", ctypes.c_int64), ("K", ctypes.c_int64), ("W", ctypes.c_int64),
                 ("rank", ctypes.c_int32), ("nlevels", ctypes.c_int32), ("lane_width", ctypes.c_int32),
@@ -122,6 +127,9 @@ def lib() -> ctypes.CDLL:
                                  ctypes.POINTER(ctypes.c_int64)],
             "hpar_parallel_for_reduce": [ctypes.c_void_p, ctypes.POINTER(ReduceDesc), ctypes.c_void_p],
             "hpar_barrier": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p],
+            "hpar_nest_resolve": [ctypes.POINTER(SyncConstruct), ctypes.c_int32, ctypes.POINTER(LevelInfo),
+                                  ctypes.POINTER(NestLevel)],
+            "hpar_level_alias": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -165,6 +173,29 @@ def hpar_hierarchy_query(device: int = 0, nccl_comm: int | None = None) -> list[
     n = ctypes.c_int32()
     _check(lib().hpar_hierarchy_query(device, nccl_comm, out, ctypes.byref(n)))
     return list(out[: n.value])
+
+
+def hpar_level_alias(name: str) -> tuple[int, int]:
+    f, l = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().hpar_level_alias(name.encode(), ctypes.byref(f), ctypes.byref(l)))
+    return f.value, l.value
+
+
+def hpar_nest_resolve(constructs: list[dict], table: list[LevelInfo]) -> list["Level"]:
+    """constructs: dicts with demand / reserve (sets of Table-2 property names),
+    schedule, loop, chunk.  Returns the resolved nest levels."""
+    n = len(constructs)
+    arr = (SyncConstruct * n)()
+    for i, c in enumerate(constructs):
+        arr[i].demand = sum(P[p] for p in c.get("demand", ()))
+        arr[i].reserve = sum(P[p] for p in c.get("reserve", ()))
+        arr[i].schedule = c.get("schedule", STATIC)
+        arr[i].loop = c.get("loop", 0)
+        arr[i].chunk = c.get("chunk", 0)
+    tab = (LevelInfo * HPAR_NLEVELS)(*table)
+    out = (NestLevel * n)()
+    _check(lib().hpar_nest_resolve(arr, n, tab, out))
+    return [Level(o.first, o.last, o.schedule, o.loop, o.chunk) for o in out]
 
 
 @dataclass
