@@ -115,4 +115,5 @@ def test_resolver_invariants_random(H, table):
             fl = flags(table, l.first, l.last)
             assert all(fl & H.P[p] for p in c["demand"])
         # the resolved nest is accepted by nest creation
-        H.Nest(lv, device=-1, desc=H.b200_desc(), nranks=8 if lv[0].first == H.HPAR_GPU else 1, clusters=4)
+        H.Nest(lv, device=-1, desc=H.b200_desc(), nranks=8 if lv[0].first == H.HPAR_GPU else 1,
+               clusters=4 if lv[0].first <= H.HPAR_CLUSTER else 0)
