@@ -215,7 +215,7 @@ def run_hpar(args):
         from inputs import gen
         rows, nnz = spec["rows"], spec["nnz"]
         off_host = gen.csr_offsets(rows, nnz)
-        nest = H.Nest(nests.c3_fast_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+        nest = H.Nest(nests.c3_fast_nest(lane_chunk=int(os.environ.get("HPAR_C3_LPL", "16"))), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
                       clusters=args.clusters)
         b, cnt = nest.shard_range(rows * world, rank)  # each rank: its own copy of the matrix (weak)
         off = torch.from_numpy(off_host).to(dev)

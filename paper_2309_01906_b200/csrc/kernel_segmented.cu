@@ -5,40 +5,52 @@
 //   GPU            static over rows                     (host: rank shard)
 //   cluster..warp  dynamic(RB) over rows: every warp of the GPU is a sibling
 //                  (collapsed level, flags = ∩ -> dynamic, atomic); a warp
-//                  claims blocks of RB consecutive rows from a GPU ticket
-//   lane           static(4) over the block's nonzeros, in 16-byte vectors
-//                  of the values array (window of 128 nonzeros per warp step)
+//                  claims blocks of RB consecutive rows (two ticket levels:
+//                  CTA chunks of CB blocks from the GPU, blocks from the CTA)
+//   lane           static(LPL) over the block's nonzeros (loop 2 = the
+//                  collapsed (row, nonzero) space), LPL = 16 (or 8): a warp
+//                  step covers a window of WIN = 32 * LPL nonzeros
 // Length class -> level (P:344-359 versioning; P:140 grainedness): a row
-// longer than L nonzeros is not reduced by its block's warp; it is split into
-// segments of S nonzeros that any warp claims from a GPU queue, and the LAST
-// segment to finish folds the row's segment partials in ascending order
-// (single-pass, wait-free: warps have no grid barrier).  Blocks never share a
-// row, so short/medium rows need no cross-warp fix-up.
+// longer than LONG nonzeros is not reduced by its block's warp; it is split
+// into segments of SEG nonzeros published in a GPU queue (one 32-byte entry
+// each, release/acquire), any warp serves them once it has no block left,
+// and the LAST segment of a row to finish folds the row's segment partials
+// in ascending order (single-pass, wait-free: warps have no grid barrier).
+// Blocks never share a row, so the other rows need no cross-warp fix-up.
 //
-// Inside a block (per warp): the block's RB+1 offsets are staged in shared
-// memory; row starts are marked as heads in a per-warp table; each 128-wide
-// window is reduced with a segmented warp scan (lane -> warp level), fp32
-// inside a window, fp64 carries across windows and for long-row segments.
-// Empty rows write 0.  Results are deterministic (fixed trees and orders).
+// Inside a block (per warp): windows are copied by TMA (one 1-D bulk copy
+// per window, lane 0 issues) into a D-deep shared-memory ring; windows lying
+// inside a long row are never fetched.  Per window the lanes build the fp64
+// exclusive prefix E of the window at even positions (lane-local pair sums
+// + warp scan); then one lane per row overlapping the window reads the
+// row's part as E[end] - E[start] (an odd end adds its one value) plus the
+// carry of a row open from the previous window.  Those differences are
+// EXACT when the window's nonzero magnitudes span at most EXACT_BINADES
+// binades: every value is then a multiple of the smallest one's ulp and each
+// prefix sum of <= 512 of them fits 53 bits.  A window failing that guard
+// (or holding Inf/NaN) takes the direct path: each row lane adds its
+// nonzeros in order in fp64.  Row results are staged in shared memory and
+// flushed with coalesced stores.  Results are deterministic.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
+#include <type_traits>
 #include "fused_common.cuh"
 
 namespace hpar {
 namespace {
 
-constexpr int RB = 256;         // rows per block claim
-constexpr int64_t LONG = 1024;  // a row with more nonzeros is split
-constexpr int64_t SEG = 8192;   // nonzeros per long-row segment
-constexpr int WARPS = 8;        // warps per CTA (all workers)
-constexpr int NV = 2;           // 16-byte vectors per lane per window
-constexpr int WIN = 128 * NV;   // nonzeros per window (lane l: 4*NV contiguous at 4*NV*l)
-constexpr int LPL = 4 * NV;     // nonzeros per lane per window
-constexpr int D = 4;            // window prefetch depth (cp.async ring)
-constexpr int LBIT = 1 << 30;   // row-id flag: a long row (its nonzeros are phase 2's)
-constexpr int CB = 32;          // row blocks per CTA claim (CTA-level dynamic chunk)
-constexpr int NSB = 8;          // ring of claimed CTA chunks
+constexpr int RB = 256;            // rows per block claim
+constexpr int64_t LONG = 4096;     // a row with more nonzeros is split
+constexpr int64_t SEG = 8192;      // nonzeros per long-row segment
+constexpr int WARPS = 8;           // warps per CTA (all workers)
+// kernel variants: LPL = nonzeros per lane per window (the nest's lane
+// static(LPL), 8 or 16), WIN = 32 * LPL per window, D = TMA ring depth
+constexpr int CB = 8;              // row blocks per CTA claim (CTA-level dynamic chunk)
+constexpr int NSB = 8;             // ring of claimed CTA chunks
+constexpr int NL = 32;             // long rows per block whose windows are skipped
+constexpr int EXACT_BINADES = 20;  // 9 (<= 512 terms) + 24 (fp32 significand) + 20 = 53
 
 struct CtaSmem {
   unsigned int ctr;            // warp-level ticket over the CTA's chunk list
@@ -47,88 +59,121 @@ struct CtaSmem {
   volatile int tag[NSB];       // j + 1 once sblock[j % NSB] is published
 };
 
+// One long-row segment in the GPU queue (32 bytes).  `row` is written last
+// (release); -1 = not yet published.  The segment's partial slot is its
+// queue index q; its row's first segment is q - k (the row's ticket slot).
+struct SegEntry {
+  long long row;
+  long long b;  // first nonzero
+  int len;      // nonzeros
+  int k;        // index within the row
+  int ns;       // segments of the row
+  int pad;
+};
+static_assert(sizeof(SegEntry) == 32, "queue entry layout");
+
 struct SegWS {
-  unsigned long long* block_ticket;  // next row block
+  unsigned long long* block_ticket;  // next row block chunk
   unsigned long long* q_tail;        // long-row segments appended
   unsigned long long* q_head;        // long-row segments claimed
   unsigned long long* blocks_done;   // row blocks finished
   unsigned long long* warps_done;    // warps exited (last one resets)
-  unsigned long long* part_next;     // partial slots allocated
-  int64_t* q_row;                    // segment -> row (-1: not yet published)
-  int32_t* q_seg;                    // segment -> index within the row
-  int64_t* q_pbase;                  // segment -> first partial slot of its row
-  double* partials;                  // per segment partial sums
-  unsigned int* tickets;             // per long row (at its pbase): segments done
+  SegEntry* q;                       // the segment queue
+  double* partials;                  // per segment partial sums (by queue index)
+  unsigned int* tickets;             // per long row (at its first segment): segments done
   int64_t q_cap;
+  unsigned long long* dbg_t;  // debug timestamps (6 per warp) or NULL
 };
+__device__ __forceinline__ long long ld_acquire_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned v) {
+  unsigned r;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
+template <typename RT, int LPL, int D>
 struct WarpSmem {
-  float4 ring[D][NV][32];  // window ring: slot, vector, lane
-  int32_t head[WIN];       // window head table: (block row + 1) | LBIT if long, 0 = none
-  int64_t off[RB + 2];     // the block's RB+1 offsets (+1 pad keeps 16-byte alignment)
+  static constexpr int WIN = 32 * LPL;
+  float ring[D][WIN];            // window ring (TMA destinations)
+  double2 E[LPL / 4][33];        // window exclusive prefix at even positions q: j = (q % LPL) / 2 in
+                                 // E[j / 2][q / LPL] (.x/.y by j % 2); q = WIN: E[0][32].x
+  int32_t off[RB + 4];           // the block's RB+1 offsets relative to base
+  RT res[RB];                    // the block's row results, flushed coalesced
+  unsigned int lmask[RB / 32];   // long rows of the block (bit per row): never flushed here
+  int32_t lrange[NL][2];         // the first NL long rows: [start, end) relative to base
+  int32_t slot_wr[D];            // window position (relative to base) held by each slot
+  uint64_t bar[D];               // ring slot "full" barriers
 };
+static_assert(RB == 256, "the flush gives each lane 8 consecutive rows");
+static_assert(sizeof(WarpSmem<float, 16, 3>) % 16 == 0 && sizeof(WarpSmem<double, 8, 4>) % 16 == 0, "TMA alignment");
 
-// 16-byte async global -> shared copy; bytes beyond src_bytes are zero-filled
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Warp segmented inclusive scan of (row, value): row >= 0 marks a lane whose
-// segment starts in it (its last head); value = its trailing sum.
-__device__ __forceinline__ void seg_scan(int& row, float& v) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int r2 = __shfl_up_sync(0xffffffffu, row, off);
-    const float v2 = __shfl_up_sync(0xffffffffu, v, off);
-    if (lane >= off && row < 0) {
-      row = r2;
-      v += v2;
-    }
-  }
+// E at an even window position q (0 <= q <= WIN)
+template <int LPL, typename W>
+__device__ __forceinline__ double e_even(const W& sm, int q) {
+  const int j = (q & (LPL - 1)) >> 1;
+  return (&sm.E[0][0].x)[(j >> 1) * 66 + (q / LPL) * 2 + (j & 1)];
 }
 
-template <bool VERIFY, bool OUT_F32>
-__global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg) {
-  extern __shared__ __align__(16) unsigned char seg_dsm[];
+__device__ __forceinline__ float max_nan_abs(float m, float v) {  // max(m, |v|), NaN propagating
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(m), "f"(fabsf(v)));
+  return r;
+}
+
+template <bool VERIFY, bool OUT_F32, int LPL, int D>
+__global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg, int long_min) {
+  using RT = typename std::conditional<OUT_F32, float, double>::type;
+  constexpr int WIN = 32 * LPL;
+  extern __shared__ __align__(128) unsigned char seg_dsm[];
   __shared__ CtaSmem cs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpSmem& sm = ((WarpSmem*)seg_dsm)[warp];
+  WarpSmem<RT, LPL, D>& sm = ((WarpSmem<RT, LPL, D>*)seg_dsm)[warp];
   if (threadIdx.x == 0) cs.ctr = 0;
   if (threadIdx.x < NSB) cs.tag[threadIdx.x] = 0;
+  if (lane < D) mbar_init(&sm.bar[lane], 1);
+  for (int i = lane; i < D * WIN; i += 32) (&sm.ring[0][0])[i] = 0.f;  // defined bytes beyond partial copies
+  fence_mbarrier_init_cluster();
+  fence_proxy_async_shared();
   __syncthreads();
   const int64_t* offs = a.offsets;
   const float* x = (const float*)a.in;
   const int64_t R = a.n0;
   const int64_t nnz_all = a.n1;
   const int64_t nblocks = (R + RB - 1) / RB;
-  const int64_t leaf = (int64_t)a.rank * a.threads_per_gpu + (int64_t)blockIdx.x * WARPS * 32 + threadIdx.x;
+  const int64_t leaf0 = (int64_t)a.rank * a.threads_per_gpu + (int64_t)blockIdx.x * WARPS * 32 + warp * 32;
+  const int64_t leaf = leaf0 + lane;
   auto write_row = [&](int64_t r, double v) {
     if constexpr (OUT_F32) ((float*)a.out)[r] = (float)v;
     else ((double*)a.out)[r] = v;
   };
-  auto cover = [&](int64_t p) {
+  auto cover_by = [&](int64_t p, int64_t who) {
     if constexpr (VERIFY) {
       if (a.verify & V_COVERAGE) {
-        a.owner[p] = leaf;
+        a.owner[p] = who;
         atomicAdd(&a.count[p], 1u);
       }
     }
   };
-  for (int i = lane; i < WIN; i += 32) sm.head[i] = 0;
-  __syncwarp();
+  const int64_t gwarp = (int64_t)blockIdx.x * WARPS + warp;
+  if (ws.dbg_t && lane == 0) ws.dbg_t[6 * gwarp] = gtimer();
+  const uint64_t pol = policy_evict_first();
 
   // ------------------------------------------------ phase 1: row blocks ----
   // Software pipeline per warp: the claim of block j+2 and the offsets of
-  // block j+1 are in flight while block j is reduced; windows are copied
-  // D ahead with cp.async into the warp's shared-memory ring.
-  // Two-level dynamic chunking: a warp takes the next block of its CTA's
-  // chunk list from a shared-memory ticket; the warp that opens chunk j
-  // claims it from the GPU ticket (CB blocks at a time) and publishes it.
+  // block j+1 are in flight while block j is reduced; windows are fetched up
+  // to D ahead.  Two-level dynamic chunking: a warp takes the next block of
+  // its CTA's chunk list from a shared-memory ticket; the warp that opens
+  // chunk j claims it from the GPU ticket (CB blocks at a time).
   const int64_t nchunks = (nblocks + CB - 1) / CB;
   auto claim = [&]() -> unsigned long long {
     long long blk = 0;
@@ -158,179 +203,362 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       offr[k] = ((int64_t)ub < nblocks && i <= nrb) ? offs[rb0 + i] : 0;
     }
   };
-  auto load4 = [&](int64_t p, int64_t lo, int64_t hi) -> float4 {
-    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (p >= lo && p + 3 < hi) {
-      t = ld_stream_f4((const float4*)(x + p));
-    } else if (p + 3 >= lo && p < hi) {
-      if (p >= lo && p < hi) t.x = x[p];
-      if (p + 1 >= lo && p + 1 < hi) t.y = x[p + 1];
-      if (p + 2 >= lo && p + 2 < hi) t.z = x[p + 2];
-      if (p + 3 >= lo && p + 3 < hi) t.w = x[p + 3];
-    }
-    return t;
-  };
   unsigned long long my_blocks = 0;  // added to blocks_done once, when this warp leaves phase 1
+  unsigned iseq = 0, cseq = 0;       // ring: windows issued / consumed by this warp
+  unsigned phases = 0;               // parity bit per ring slot
+  const int64_t nnz4 = nnz_all & ~(int64_t)3;
+  auto ring_wait = [&]() -> int {  // next issued window: its slot, once landed
+    const int s = (int)(cseq % D);
+    mbar_wait(&sm.bar[s], (phases >> s) & 1u);
+    phases ^= 1u << s;
+    ++cseq;
+    return s;
+  };
+  // One published long-row segment: its nonzeros stream through the ring
+  // (fp32 per lane and window, fp64 across); the row's LAST segment to
+  // finish folds the segment partials in ascending order.
+  auto do_segment = [&](unsigned long long q) {
+    long long row = -1, b = 0;
+    int len = 0, k = 0, ns = 0;
+    if (lane == 0) {
+      SegEntry& en = ws.q[q];
+      while ((row = ld_acquire_s64(&en.row)) < 0) __nanosleep(32);
+      b = en.b;
+      len = en.len;
+      k = en.k;
+      ns = en.ns;
+      en.row = -1;  // self-reset for the next call
+    }
+    row = __shfl_sync(0xffffffffu, row, 0);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    len = __shfl_sync(0xffffffffu, len, 0);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    ns = __shfl_sync(0xffffffffu, ns, 0);
+    const int64_t pb = (int64_t)q - k;
+    const int64_t e = b + len;
+    const int64_t sb = b & ~(int64_t)3;  // 16-byte aligned origin; positions below relative to it
+    const int n = (dbg & 1) ? 0 : (int)(e - sb);
+    const int64_t e4 = (e + 3) & ~(int64_t)3;
+    const int c4 = (int)((e4 < nnz4 ? e4 : nnz4) - sb);  // copied by TMA; beyond: the array's tail
+    const int bo = (int)(b - sb);
+    auto seg_issue = [&](int w) {
+      const int s = (int)(iseq % D);
+      if (lane == 0) {
+        sm.slot_wr[s] = w;
+        const int m = (c4 - w < WIN) ? c4 - w : WIN;
+        if (m > 0) {
+          mbar_arrive_expect_tx(&sm.bar[s], (uint32_t)m * 4u);
+          bulk_g2s(&sm.ring[s][0], x + sb + w, (uint32_t)m * 4u, &sm.bar[s], pol);
+        } else {
+          mbar_arrive(&sm.bar[s]);
+        }
+      }
+      ++iseq;
+    };
+    int iw = 0;
+    for (int d = 0; d < D && iw < n; ++d, iw += WIN) seg_issue(iw);
+    double acc = 0.0;
+    while (cseq != iseq) {
+      const int s = ring_wait();
+      const int wr = sm.slot_wr[s];
+      const int p = wr + LPL * lane;
+      float v[LPL];
+#pragma unroll
+      for (int j = 0; j < LPL / 4; ++j) {
+        const float4 t = *(const float4*)&sm.ring[s][LPL * lane + 4 * j];
+        v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
+      }
+      if (wr == 0 || wr + WIN > n) {  // segment edges; the array's unaligned tail
+#pragma unroll
+        for (int j = 0; j < LPL; ++j) {
+          const int q2 = p + j;
+          if (q2 >= c4 && q2 < n) v[j] = x[sb + q2];
+          if (q2 < bo || q2 >= n) v[j] = 0.f;
+        }
+      }
+      float t4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t4[j] = (v[4 * j] + v[4 * j + 1]) + (v[4 * j + 2] + v[4 * j + 3]);
+      acc += (double)((t4[0] + t4[1]) + (t4[2] + t4[3]));
+      if constexpr (VERIFY) {
+        for (int j = 0; j < LPL; ++j)
+          if (p + j >= bo && p + j < n) cover_by(sb + p + j, leaf);
+      }
+      __syncwarp();  // slot s is free again
+      if (iw < n) {
+        seg_issue(iw);
+        iw += WIN;
+      }
+    }
+    acc = warp_fold<OP_SUM>(acc);
+    if (lane == 0) {
+      __stcg(&ws.partials[q], acc);
+      const unsigned t = atom_add_acq_rel_u32(&ws.tickets[pb], 1u);  // release my partial
+      if ((int)t == ns - 1) {  // last segment of the row: ordered fold (acquired)
+        double tot = 0.0;
+        for (int j = 0; j < ns; ++j) tot += __ldcg(&ws.partials[pb + j]);
+        write_row(row, tot);
+        ws.tickets[pb] = 0u;
+      }
+    }
+  };
+  // Long-row segments interleave with the row blocks: each warp holds one
+  // claimed queue ticket and serves it between blocks once it is published.
+  constexpr unsigned long long NONE = ~0ull;
+  unsigned long long myq = NONE;
+  auto claim_seg = [&]() {
+    if (myq == NONE) {
+      unsigned long long q = 0;
+      if (lane == 0) q = atomicAdd(ws.q_head, 1ull);
+      myq = __shfl_sync(0xffffffffu, q, 0);
+    }
+  };
   unsigned long long u = claim();
   load_offs(u);
   while ((int64_t)u < nblocks) {
     const unsigned long long u1 = claim();
     const int64_t r0 = (int64_t)u * RB;
     const int nr = (int)((R - r0 < RB) ? (R - r0) : RB);
+    // window origin: 64-byte aligned; positions below are 32-bit, relative to
+    // it (nnz < 2^31 per rank)
+    const int64_t base = __shfl_sync(0xffffffffu, offr[0], 0) & ~(int64_t)15;
 #pragma unroll
     for (int k = 0; k < (RB + 1 + 31) / 32; ++k) {
       const int i = lane + 32 * k;
-      if (i <= nr) sm.off[i] = offr[k];
+      if (i <= nr) sm.off[i] = (int)(offr[k] - base);
     }
+#pragma unroll
+    for (int k = 0; k < (int)(RB * sizeof(RT)) / 16 / 32; ++k)
+      ((float4*)sm.res)[lane + 32 * k] = make_float4(0.f, 0.f, 0.f, 0.f);  // empty rows stay 0
     __syncwarp();
     load_offs(u1);  // next block's offsets, in flight during this block
-    const int64_t P0 = sm.off[0], P1 = sm.off[nr];
-    // long rows: enqueue their segments; empty rows: 0
-    bool my_long = false;
-    for (int i = lane; i < nr; i += 32) {
-      const int64_t len = sm.off[i + 1] - sm.off[i];
-      if (len == 0) write_row(r0 + i, 0.0);
-      if (len > LONG) {
-        my_long = true;
-        const int64_t ns = (len + SEG - 1) / SEG;
-        const unsigned long long q = atomicAdd(ws.q_tail, (unsigned long long)ns);
-        const unsigned long long pb = atomicAdd(ws.part_next, (unsigned long long)ns);
-        for (int64_t k = 0; k < ns; ++k) {
-          ws.q_seg[q + k] = (int32_t)k;
-          ws.q_pbase[q + k] = (int64_t)pb;
+    const int p0 = sm.off[0], p1 = sm.off[nr];
+    // long rows: enqueue their segments, mark them, list the first NL
+    int nl = 0;
+#pragma unroll
+    for (int k = 0; k < RB / 32; ++k) {
+      const int i = lane + 32 * k;
+      bool lg = false;
+      int s_ = 0, e_ = 0;
+      if (i < nr) {
+        s_ = sm.off[i];
+        e_ = sm.off[i + 1];
+        lg = e_ - s_ > long_min;
+        if (lg) {
+          const int len = e_ - s_;
+          const int ns = (int)((len + SEG - 1) / SEG);
+          const unsigned long long q = atomicAdd(ws.q_tail, (unsigned long long)ns);
+          for (int j = 0; j < ns; ++j) {
+            SegEntry& en = ws.q[q + j];
+            en.b = base + s_ + (int64_t)j * SEG;
+            en.len = (len - j * SEG < SEG) ? len - j * SEG : (int)SEG;
+            en.k = j;
+            en.ns = ns;
+          }
+          fence_acq_rel_gpu();  // entries before their publication
+          for (int j = 0; j < ns; ++j) *(volatile long long*)&ws.q[q + j].row = r0 + i;
         }
-        __threadfence();  // entries before their publication
-        for (int64_t k = 0; k < ns; ++k) *(volatile int64_t*)&ws.q_row[q + k] = r0 + i;
       }
+      const unsigned m = __ballot_sync(0xffffffffu, lg);
+      if (lane == 0) sm.lmask[k] = m;
+      if (lg) {
+        const int at = nl + __popc(m & ((1u << lane) - 1u));
+        if (at < NL) {
+          sm.lrange[at][0] = s_;
+          sm.lrange[at][1] = e_;
+        }
+      }
+      nl += __popc(m);
     }
-    const bool had_long = __any_sync(0xffffffffu, my_long);
-    // windows of WIN nonzeros, 16-byte aligned.  Every non-empty row starting
-    // in a window is a head; long rows are heads too (they close the previous
-    // row) but carry LBIT and are never written here.  Positions inside the
-    // window loop are 32-bit, relative to `base` (nnz < 2^31 per rank).
-    const int64_t base = P0 & ~(int64_t)15;
-    const float* xb = x + base;
-    const int p0 = (int)(P0 - base), p1 = (int)(P1 - base);
+    nl = nl < NL ? nl : NL;
+    __syncwarp();
+
+    // window fetch: bytes up to p1 (rounded to 16) but never past the last
+    // whole 16 bytes of the array; the <= 3 nonzeros beyond are loaded directly
     const int64_t lim64 = nnz_all - base;
-    const int lim = lim64 > 0x7FFFFFF0 ? 0x7FFFFFF0 : (int)lim64;  // readable nonzeros from base
-    auto issue = [&](int wr, int slot) {  // copy window at relative position wr
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int p = wr + LPL * lane + 4 * v;
-        const int bytes = (p + 4 <= lim) ? 16 : (p < lim ? (lim - p) * 4 : 0);
-        cp_async16(&sm.ring[slot][v][lane], xb + (bytes ? p : 0), bytes);
+    const int lim = lim64 > 0x7FFFFFF0 ? 0x7FFFFFF0 : (int)lim64;
+    const int lim4 = lim & ~3;
+    const int p1c = ((p1 + 3) & ~3) < lim4 ? ((p1 + 3) & ~3) : lim4;
+    int li = 0;  // issuer's cursor over the long-row list
+    auto skip = [&](int w) -> int {  // first window at or after w not inside a long row
+      while (li < nl) {
+        const int ls = sm.lrange[li][0], le = sm.lrange[li][1];
+        if (le <= w) {
+          ++li;
+        } else if (ls <= w && w + WIN <= le) {
+          w = le & ~(WIN - 1);
+        } else {
+          break;
+        }
       }
-      cp_async_commit();
+      return w;
     };
-    int cur = 0;           // next block row whose start is not yet marked
-    int open_row = -1;     // (block row | LBIT) of the open segment, -1: none
-    double carry = 0.0;    // fp64 sum of the open row before this window
-    int slot = 0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) issue(WIN * i, i);
-    for (int wr = (dbg & 2) ? p1 : 0; wr < p1; wr += WIN) {
-      // inside a long row with no head ahead in this window: skip to the window
-      // holding the next row start (the long row's nonzeros are phase 2's)
-      if (open_row >= 0 && (open_row & LBIT)) {
-        const int nxt = (cur < nr) ? (int)(sm.off[cur] - base) : p1;
-        if (nxt >= wr + WIN) {
-          wr = (nxt / WIN) * WIN;
-          if (wr >= p1) break;
-          cp_async_wait<0>();
-          slot = 0;
-#pragma unroll
-          for (int i = 0; i < D; ++i) issue(wr + WIN * i, i);
+    auto issue = [&](int w) {
+      const int s = (int)(iseq % D);
+      if (lane == 0) {
+        sm.slot_wr[s] = w;
+        const int n = (p1c - w < WIN) ? p1c - w : WIN;
+        if (n > 0) {
+          mbar_arrive_expect_tx(&sm.bar[s], (uint32_t)n * 4u);
+          bulk_g2s(&sm.ring[s][0], x + base + w, (uint32_t)n * 4u, &sm.bar[s], pol);
+        } else {
+          mbar_arrive(&sm.bar[s]);
         }
       }
+      ++iseq;
+    };
+    int iw = (dbg & 2) ? p1 : skip(0);
+    for (int d = 0; d < D && iw < p1; ++d) {
+      issue(iw);
+      iw = skip(iw + WIN);
+    }
+    int rcur = 0;        // first row overlapping the next window
+    double carry = 0.0;  // row rcur's sum before the next window
+    while (cseq != iseq) {
+      const int s = (int)(cseq % D);
+      mbar_wait(&sm.bar[s], (phases >> s) & 1u);
+      phases ^= 1u << s;
+      ++cseq;
+      const int wr = sm.slot_wr[s];
       const int wend = wr + WIN;
-      // mark heads: non-empty rows starting in [wr, wend)
-      while (cur < nr && (int)(sm.off[cur] - base) < wend) {
-        const int i = cur + lane;
-        bool in = false;
-        if (i < nr) {
-          const int s_ = (int)(sm.off[i] - base), e_ = (int)(sm.off[i + 1] - base);
-          in = s_ < wend;
-          if (in && e_ > s_) sm.head[s_ - wr] = (i + 1) | ((e_ - s_ > LONG) ? LBIT : 0);
-        }
-        cur += __popc(__ballot_sync(0xffffffffu, in));
-      }
-      __syncwarp();
-      // this lane's LPL nonzeros (copied D windows ago); refill the slot
       const int p = wr + LPL * lane;
-      cp_async_wait<D - 1>();
       float v[LPL];
 #pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        const float4 t = sm.ring[slot][q][lane];
-        v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+      for (int j = 0; j < LPL / 4; ++j) {
+        const float4 t = *(const float4*)&sm.ring[s][LPL * lane + 4 * j];
+        v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
       }
-      issue(wr + WIN * D, slot);
-      slot = (slot + 1 == D) ? 0 : slot + 1;
-      if (p < p0 || p + LPL > p1) {
-#pragma unroll
-        for (int k = 0; k < LPL; ++k)
-          if (p + k < p0 || p + k >= p1) v[k] = 0.f;  // neighbours' nonzeros
-      }
-      int h[LPL];
-#pragma unroll
-      for (int q = 0; q < LPL / 4; ++q) {
-        const int4 hq = *(const int4*)&sm.head[LPL * lane + 4 * q];
-        h[4 * q] = hq.x; h[4 * q + 1] = hq.y; h[4 * q + 2] = hq.z; h[4 * q + 3] = hq.w;
-        *(int4*)&sm.head[LPL * lane + 4 * q] = make_int4(0, 0, 0, 0);
-      }
-      // lane-local segmented sums (branch-free); rows entirely inside the
-      // lane are written when their successor's head is met
-      float pre = 0.f;   // before the first head: belongs to the open row
-      float tail = 0.f;  // from the last head on
-      int last = -1;     // (block row | LBIT) of the last head in this lane
-#pragma unroll
-      for (int k = 0; k < LPL; ++k) {
-        const bool hk = h[k] != 0;
-        if (hk && last >= 0 && !(last & LBIT)) write_row(r0 + last, (double)tail);
-        last = hk ? h[k] - 1 : last;
-        tail = hk ? 0.f : tail;
-        const bool in_open = last < 0;
-        pre = in_open ? pre + v[k] : pre;
-        tail = in_open ? tail : tail + v[k];
-      }
-      // lane -> warp: segmented scan of (last head row, trailing value)
-      int srow = last;
-      float sval = (last >= 0) ? tail : pre;
-      seg_scan(srow, sval);
-      int erow = __shfl_up_sync(0xffffffffu, srow, 1);
-      float eval = __shfl_up_sync(0xffffffffu, sval, 1);
-      if (lane == 0) { erow = -1; eval = 0.f; }
-      const int prev = (erow >= 0) ? erow : open_row;  // row of the nonzeros before the first head
-      // the row open before this lane's first head ends there
-      if (last >= 0 && prev >= 0 && !(prev & LBIT)) {
-        const double tot = (erow >= 0) ? (double)(eval + pre) : carry + (double)eval + (double)pre;
-        write_row(r0 + prev, tot);
-      }
-      if constexpr (VERIFY) {
-        int row = prev;
+      // Positions outside [p0, p1) hold neighbours' (or stale) values: no row
+      // range covers them, so they cancel in every E difference once E is
+      // exact; the guard below sees them too (conservative).  The array's
+      // unaligned tail (< 4 nonzeros past the last whole 16 bytes) is read
+      // directly.
+      if (wend > lim4 && p1 > lim4) {
 #pragma unroll
         for (int k = 0; k < LPL; ++k) {
-          if (h[k]) row = h[k] - 1;
-          if (p + k >= p0 && p + k < p1 && row >= 0 && !(row & LBIT)) cover(base + p + k);
+          const int q = p + k;
+          if (q >= lim4 && q < p1) v[k] = x[base + q];
         }
       }
-      // window end: the trailing open segment carries into the next window
-      const int trow = __shfl_sync(0xffffffffu, srow, 31);
-      const float tval = __shfl_sync(0xffffffffu, sval, 31);
-      if (trow >= 0) {
-        open_row = trow;
-        carry = (double)tval;
-      } else {
-        carry += (double)tval;
+      // exactness guard: binade span of the window's nonzero magnitudes
+      float amax = 0.f;
+      unsigned umin = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < LPL; ++k) {
+        amax = max_nan_abs(amax, v[k]);
+        const unsigned t = __float_as_uint(v[k]) * 2u - 1u;  // |v| bits << 1, minus 1: zero -> max
+        umin = t < umin ? t : umin;
+      }
+      const unsigned gmax = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));
+      const unsigned gmin = __reduce_min_sync(0xffffffffu, umin);
+      const int emax = (int)(gmax >> 23), emin = (int)((gmin + 1u) >> 24);
+      const bool exact = emax < 255 && emax - emin <= EXACT_BINADES;
+      if (exact) {
+        // lane-local prefix at even positions: pair sums, then their prefix
+        // in two independent halves (short dependency chains)
+        double c[LPL / 2];  // c[j] = v[0] + ... + v[2j+1]
+#pragma unroll
+        for (int j = 0; j < LPL / 2; ++j) c[j] = (double)v[2 * j] + (double)v[2 * j + 1];
+#pragma unroll
+        for (int j = 1; j < LPL / 4; ++j) {
+          c[j] += c[j - 1];
+          c[LPL / 4 + j] += c[LPL / 4 + j - 1];
+        }
+#pragma unroll
+        for (int j = LPL / 4; j < LPL / 2; ++j) c[j] += c[LPL / 4 - 1];
+        double incl = c[LPL / 2 - 1];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        double ex = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) ex = 0.0;
+        sm.E[0][lane] = make_double2(ex, ex + c[0]);
+#pragma unroll
+        for (int k = 1; k < LPL / 4; ++k) sm.E[k][lane] = make_double2(ex + c[2 * k - 1], ex + c[2 * k]);
+        if (lane == 31) sm.E[0][32].x = incl;
+        __syncwarp();
+      }
+      // one lane per row overlapping the window, 32 rows per step
+      int r = rcur;
+      for (;;) {
+        const int i = r + lane;
+        const bool valid = i < nr && sm.off[i] < wend;
+        double val = 0.0;
+        bool complete = false;
+        if (valid) {
+          const int s_ = sm.off[i], e_ = sm.off[i + 1];
+          // clamped: a long row whose windows were skipped may end before wr
+          const int sc = min(max(s_ - wr, 0), WIN);
+          const int ec = min(max(e_ - wr, sc), WIN);
+          if (exact) {
+            val = (e_even<LPL>(sm, ec & ~1) - e_even<LPL>(sm, sc & ~1)) +
+                  ((double)((ec & 1) ? sm.ring[s][ec - 1] : 0.f) - (double)((sc & 1) ? sm.ring[s][sc - 1] : 0.f));
+          } else {
+            for (int q = sc; q < ec; ++q) val += (double)((wr + q >= lim4) ? x[base + wr + q] : sm.ring[s][q]);
+          }
+          if (s_ < wr) val += carry;  // the row open from the previous window
+          complete = e_ <= wend;
+          const bool lg = (sm.lmask[i >> 5] >> (i & 31)) & 1u;
+          if (complete && !lg) sm.res[i] = (RT)val;
+          if constexpr (VERIFY) {
+            if (!lg)
+              for (int q = sc; q < ec; ++q) cover_by(base + wr + q, leaf0 + q / LPL);
+          }
+        }
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        const unsigned cm = __ballot_sync(0xffffffffu, complete);
+        const int cnt = __popc(vm);
+        if (cnt == 0) break;
+        if (!((cm >> (cnt - 1)) & 1u)) {  // the last overlapping row continues
+          carry = __shfl_sync(0xffffffffu, val, cnt - 1);
+          rcur = r + cnt - 1;
+          break;
+        }
+        r += cnt;
+        rcur = r;
+        carry = 0.0;
+        if (cnt < 32) break;
+      }
+      __syncwarp();  // E and ring slot s are free again
+      if (iw < p1) {
+        issue(iw);
+        iw = skip(iw + WIN);
       }
     }
-    cp_async_wait<0>();  // the ring is reused by the next block
-    // the last open row of the block ends at P1
-    if (lane == 0 && open_row >= 0 && !(open_row & LBIT)) write_row(r0 + open_row, carry);
+    // flush: lane l writes rows 8l..8l+7 (long rows excluded)
+    {
+      const int rl = 8 * lane;
+      const unsigned lm = (sm.lmask[lane >> 2] >> ((lane & 3) * 8)) & 0xFFu;
+      RT* o = (RT*)a.out + r0 + rl;
+      if (rl + 8 <= nr && lm == 0 && ((uintptr_t)a.out & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < (int)(8 * sizeof(RT)) / 16; ++q) ((float4*)o)[q] = ((const float4*)(sm.res + rl))[q];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (rl + j < nr && !((lm >> j) & 1u)) o[j] = sm.res[rl + j];
+      }
+    }
     __syncwarp();
-    if (had_long && lane == 0) __threadfence();  // queue entries visible before blocks_done says so
     ++my_blocks;
     u = u1;
+    if (dbg & 4) {  // (knob) serve published segments between blocks
+      for (;;) {
+        unsigned long long head = 0, tail = 0;
+        if (lane == 0) {
+          tail = *(volatile unsigned long long*)ws.q_tail;
+          head = *(volatile unsigned long long*)ws.q_head;
+        }
+        tail = __shfl_sync(0xffffffffu, tail, 0);
+        head = __shfl_sync(0xffffffffu, head, 0);
+        if (myq == NONE && head < tail) claim_seg();
+        if (myq == NONE || myq >= tail) break;
+        do_segment(myq);
+        myq = NONE;
+      }
+    }
   }
 
   if (lane == 0) {
@@ -338,81 +566,51 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     atomicAdd(ws.blocks_done, my_blocks);
   }
 
-  // -------------------------------------------- phase 2: long-row segments ----
+  if (ws.dbg_t && lane == 0) ws.dbg_t[6 * gwarp + 1] = gtimer();
+  // ------------------------------- phase 2: the remaining long-row segments ----
+  // Claim a ticket only while the queue looks non-empty; a ticket that lost
+  // the race waits for its entry.  Leave once every block is done (no entry
+  // can appear any more) and the queue is drained.  Idle polling backs off.
+  unsigned nap = 32;
+  unsigned long long dbg_nseg = 0, dbg_tseg = 0, dbg_tdone = 0;
   for (;;) {
-    unsigned long long q = 0;
-    if (lane == 0) q = atomicAdd(ws.q_head, 1ull);
-    q = __shfl_sync(0xffffffffu, q, 0);
-    // wait until segment q exists, or until no segment can appear any more
-    bool have = false;
-    for (;;) {
-      unsigned long long tail = 0, done = 0;
+    unsigned long long head = 0, tail = 0, done = 0;
+    if (lane == 0) {
+      tail = *(volatile unsigned long long*)ws.q_tail;
+      head = *(volatile unsigned long long*)ws.q_head;
+      done = *(volatile unsigned long long*)ws.blocks_done;
+    }
+    tail = __shfl_sync(0xffffffffu, tail, 0);
+    head = __shfl_sync(0xffffffffu, head, 0);
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (myq == NONE && head < tail) claim_seg();
+    if (myq != NONE && myq < tail) {
+      const unsigned long long t0 = ws.dbg_t ? gtimer() : 0;
+      do_segment(myq);
+      if (ws.dbg_t) { ++dbg_nseg; dbg_tseg += gtimer() - t0; }
+      myq = NONE;
+      nap = 32;
+      continue;
+    }
+    if ((int64_t)done >= nblocks) {
+      if (ws.dbg_t && !dbg_tdone) dbg_tdone = gtimer();
+      // every entry is published before blocks_done counts its block
+      __threadfence();
       if (lane == 0) {
         tail = *(volatile unsigned long long*)ws.q_tail;
-        done = *(volatile unsigned long long*)ws.blocks_done;
+        head = *(volatile unsigned long long*)ws.q_head;
       }
       tail = __shfl_sync(0xffffffffu, tail, 0);
-      done = __shfl_sync(0xffffffffu, done, 0);
-      if (q < tail) { have = true; break; }
-      if ((int64_t)done >= nblocks) {
-        __threadfence();
-        if (lane == 0) tail = *(volatile unsigned long long*)ws.q_tail;
-        tail = __shfl_sync(0xffffffffu, tail, 0);
-        have = q < tail;
-        break;
-      }
-      __nanosleep(200);
+      head = __shfl_sync(0xffffffffu, head, 0);
+      if (myq != NONE ? myq < tail : head < tail) continue;
+      break;
     }
-    if (!have) break;
-    int64_t row = -1;
-    if (lane == 0) {
-      while ((row = *(volatile int64_t*)&ws.q_row[q]) < 0) __nanosleep(64);
-      ws.q_row[q] = -1;  // self-reset for the next call
-    }
-    row = __shfl_sync(0xffffffffu, row, 0);
-    __threadfence();
-    const int32_t k = *(volatile int32_t*)&ws.q_seg[q];
-    const int64_t pb = *(volatile int64_t*)&ws.q_pbase[q];
-    const int64_t s0 = offs[row], e0 = offs[row + 1];
-    const int64_t ns = (e0 - s0 + SEG - 1) / SEG;
-    const int64_t b = s0 + (int64_t)k * SEG;
-    const int64_t e = (b + SEG < e0) ? b + SEG : e0;
-    double acc = 0.0;
-    {
-      constexpr int D2 = 8;
-      int64_t wb = (dbg & 1) ? e : (b & ~(int64_t)3);
-      for (; wb < e; wb += 128 * D2) {
-        float4 t[D2];
-#pragma unroll
-        for (int i = 0; i < D2; ++i) t[i] = load4(wb + 128 * i + 4 * lane, b, e);
-        float s = 0.f;
-#pragma unroll
-        for (int i = 0; i < D2; ++i) s += (t[i].x + t[i].y) + (t[i].z + t[i].w);
-        acc += (double)s;
-        if constexpr (VERIFY) {
-          for (int i = 0; i < D2; ++i)
-            for (int j = 0; j < 4; ++j) {
-              const int64_t pp = wb + 128 * i + 4 * lane + j;
-              if (pp >= b && pp < e) cover(pp);
-            }
-        }
-      }
-    }
-    acc = warp_fold<OP_SUM>(acc);
-    if (lane == 0) {
-      ws.partials[pb + k] = acc;
-      __threadfence();
-      const unsigned t = atomicAdd(&ws.tickets[pb], 1u);
-      if ((int64_t)t == ns - 1) {  // last segment of the row: ordered fold
-        __threadfence();
-        double tot = 0.0;
-        for (int64_t j = 0; j < ns; ++j) tot += *(volatile double*)&ws.partials[pb + j];
-        write_row(row, tot);
-        ws.tickets[pb] = 0u;
-      }
-    }
+    __nanosleep(nap);
+    nap = nap < 2048 ? 2 * nap : 2048;
   }
 
+  if (ws.dbg_t && lane == 0) ws.dbg_t[6 * gwarp + 2] = gtimer();
+  if (ws.dbg_t && lane == 0) { ws.dbg_t[6 * gwarp + 3] = dbg_nseg; ws.dbg_t[6 * gwarp + 4] = dbg_tseg; ws.dbg_t[6 * gwarp + 5] = dbg_tdone; }
   // --------------------------------------------- exit: last warp resets ----
   if (lane == 0) {
     __threadfence();
@@ -422,7 +620,6 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       *ws.q_tail = 0ull;
       *ws.q_head = 0ull;
       *ws.blocks_done = 0ull;
-      *ws.part_next = 0ull;
       __threadfence();
       *ws.warps_done = 0ull;
     }
@@ -436,12 +633,12 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
 static int64_t max_segments(int64_t nnz) { return nnz / SEG + nnz / LONG + 64; }
 
 size_t segmented_ws_bytes(int64_t nnz) {
-  return 64 * 8 + (size_t)max_segments(nnz) * (8 + 8 + 8 + 4 + 4) + 4096;
+  return 64 * 8 + (size_t)max_segments(nnz) * (sizeof(SegEntry) + 8 + 4) + 4096;
 }
-// byte offset and length of the q_row array (initialised to -1 = empty)
+// byte offset and length of the queue (initialised to all-ones: row = -1 = empty)
 void segmented_ws_qrow(int64_t nnz, size_t* off, size_t* len) {
   *off = 64 * 8;
-  *len = (size_t)max_segments(nnz) * 8;
+  *len = (size_t)max_segments(nnz) * sizeof(SegEntry);
 }
 
 bool segmented_matches(const NestArgs& a, const char** why) {
@@ -452,11 +649,11 @@ bool segmented_matches(const NestArgs& a, const char** why) {
   if (v.n != 2) { *why = "needs [cluster..warp dynamic(RB) rows] [lane static(4) positions]"; return false; }
   const DevLevel *t = v.l[0], *l = v.l[1];
   if (t->sfirst != S_CLUSTER || t->slast != S_WARP || t->sched != SCHED_DYNAMIC || t->chunk != RB || t->loop != 0) {
-    *why = "teams-warps level must be dynamic(128) over rows";
+    *why = "teams-warps level must be dynamic(256) over rows";
     return false;
   }
-  if (!is_level(l, S_LANE) || l->sched != SCHED_STATIC_CHUNK || l->chunk != 4 * NV || l->loop != 2) {
-    *why = "lane level must be static(8) over the collapsed nonzeros (loop 2)";
+  if (!is_level(l, S_LANE) || l->sched != SCHED_STATIC_CHUNK || (l->chunk != 8 && l->chunk != 16) || l->loop != 2) {
+    *why = "lane level must be static(8) or static(16) over the collapsed nonzeros (loop 2)";
     return false;
   }
   if (a.radix[S_WARP] != WARPS) { *why = "W must be 8"; return false; }
@@ -475,18 +672,21 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
   ws.q_head = ws.block_ticket + 2;
   ws.blocks_done = ws.block_ticket + 3;
   ws.warps_done = ws.block_ticket + 4;
-  ws.part_next = ws.block_ticket + 5;
   p += 64 * 8;
-  ws.q_row = (int64_t*)p;
-  p += maxseg * 8;
-  ws.q_pbase = (int64_t*)p;
-  p += maxseg * 8;
+  ws.q = (SegEntry*)p;
+  p += maxseg * sizeof(SegEntry);
   ws.partials = (double*)p;
   p += maxseg * 8;
-  ws.q_seg = (int32_t*)p;
-  p += maxseg * 4;
   ws.tickets = (unsigned int*)p;
   ws.q_cap = maxseg;
+  ws.dbg_t = nullptr;
+  static unsigned long long* dbg_buf = nullptr;
+  const bool times = getenv("HPAR_SEG_TIMES") != nullptr;
+  const int64_t nwarps = a.C * a.K * WARPS;
+  if (times) {
+    if (!dbg_buf) cudaMalloc(&dbg_buf, nwarps * 6 * 8);
+    ws.dbg_t = dbg_buf;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.C * a.K));
   cfg.blockDim = dim3(WARPS * 32);
@@ -498,18 +698,65 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cfg.dynamicSmemBytes = WARPS * sizeof(WarpSmem);
-  auto pick = [&](auto kern) -> cudaError_t {
+  const bool f32 = a.out_dtype == DT_F32;
+  auto pick = [&](auto kern, size_t warp_smem) -> cudaError_t {
+    cfg.dynamicSmemBytes = WARPS * warp_smem;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)cfg.dynamicSmemBytes);
     if (e != cudaSuccess) return e;
+    // every CTA must be co-resident (no CTA may start after others exit):
+    // clamp the grid to the clusters that fit at once
+    int fit = 0;
+    e = cudaOccupancyMaxActiveClusters(&fit, kern, &cfg);
+    if (e != cudaSuccess) return e;
+    if (fit > 0 && (int64_t)fit < a.C) cfg.gridDim = dim3((unsigned)(fit * a.K));
     static int dbg = -1;
     if (dbg < 0) dbg = getenv("HPAR_SEG_DEBUG") ? atoi(getenv("HPAR_SEG_DEBUG")) : 0;
-    return cudaLaunchKernelEx(&cfg, kern, a, ws, dbg);
+    static int lmin = -1;
+    if (lmin < 0) lmin = getenv("HPAR_SEG_LONG") ? atoi(getenv("HPAR_SEG_LONG")) : (int)LONG;
+    if (lmin < (int)LONG) lmin = (int)LONG;  // the queue is sized for rows > LONG
+    return cudaLaunchKernelEx(&cfg, kern, a, ws, dbg, lmin);
   };
-  const bool f32 = a.out_dtype == DT_F32;
-  if (a.verify) return f32 ? pick(segmented_kernel<true, true>) : pick(segmented_kernel<true, false>);
-  return f32 ? pick(segmented_kernel<false, true>) : pick(segmented_kernel<false, false>);
+  // variant: LPL from the nest's lane chunk; ring depth D (HPAR_SEG_D knob)
+  const int lpl = device_levels(a).l[1]->chunk;
+  static int dknob = -1;
+  if (dknob < 0) dknob = getenv("HPAR_SEG_D") ? atoi(getenv("HPAR_SEG_D")) : 0;
+  auto launch_v = [&](auto lpl_c, auto d_c) -> cudaError_t {
+    constexpr int L = decltype(lpl_c)::value, DD = decltype(d_c)::value;
+    if (a.verify)
+      return f32 ? pick(segmented_kernel<true, true, L, DD>, sizeof(WarpSmem<float, L, DD>))
+                 : pick(segmented_kernel<true, false, L, DD>, sizeof(WarpSmem<double, L, DD>));
+    return f32 ? pick(segmented_kernel<false, true, L, DD>, sizeof(WarpSmem<float, L, DD>))
+               : pick(segmented_kernel<false, false, L, DD>, sizeof(WarpSmem<double, L, DD>));
+  };
+  using I8 = std::integral_constant<int, 8>;
+  using I16 = std::integral_constant<int, 16>;
+  using I2 = std::integral_constant<int, 2>;
+  using I3 = std::integral_constant<int, 3>;
+  using I4 = std::integral_constant<int, 4>;
+  cudaError_t er;
+  if (lpl == 16) er = (dknob == 3) ? launch_v(I16(), I3()) : launch_v(I16(), I2());
+  else er = (dknob == 3) ? launch_v(I8(), I3()) : launch_v(I8(), I4());
+  if (times && er == cudaSuccess) {  // debug only: per-warp phase times
+    cudaStreamSynchronize(s);
+    const int64_t nwarps = (int64_t)cfg.gridDim.x * WARPS;
+    unsigned long long* h = (unsigned long long*)malloc(nwarps * 48);
+    cudaMemcpy(h, dbg_buf, nwarps * 48, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, tmax = 0;
+    for (int64_t w = 0; w < nwarps; ++w) { if (h[6 * w] < t0) t0 = h[6 * w]; if (h[6 * w + 2] > tmax) tmax = h[6 * w + 2]; }
+    double s1 = 0, s2 = 0, st = 0, p1max = 0, p1min = 1e30, nseg = 0, tseg = 0, tdone = 0, tdmin = 1e30;
+    for (int64_t w = 0; w < nwarps; ++w) {
+      const double a0 = (h[6 * w] - t0) * 1e-3, a1 = (h[6 * w + 1] - t0) * 1e-3, a2 = (h[6 * w + 2] - t0) * 1e-3;
+      st += a0; s1 += a1; s2 += a2; if (a1 > p1max) p1max = a1; if (a1 < p1min) p1min = a1;
+      nseg += h[6 * w + 3]; tseg += h[6 * w + 4] * 1e-3;
+      const double td = h[6 * w + 5] ? (h[6 * w + 5] - t0) * 1e-3 : 0; tdone += td; if (td > 0 && td < tdmin) tdmin = td;
+    }
+    fprintf(stderr, "seg times (us): start avg %.1f | phase1 end avg %.1f min %.1f max %.1f | exit avg %.1f max %.1f"
+            " | phase2 segs/warp %.2f, us/seg %.2f, all-blocks-done seen avg %.1f min %.1f\n",
+            st / nwarps, s1 / nwarps, p1min, p1max, s2 / nwarps, (tmax - t0) * 1e-3, nseg / nwarps, tseg / (nseg > 0 ? nseg : 1), tdone / nwarps, tdmin);
+    free(h);
+  }
+  return er;
 }
 
 }  // namespace hpar

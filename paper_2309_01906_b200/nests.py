@@ -77,18 +77,18 @@ def c3_nest(with_gpu: bool = True, rows_chunk: int = 64, width: int = 8) -> list
     return lv
 
 
-def c3_fast_nest(with_gpu: bool = True, rows_chunk: int = 256) -> list[Level]:
+def c3_fast_nest(with_gpu: bool = True, rows_chunk: int = 256, lane_chunk: int = 16) -> list[Level]:
     """Config 3 (the fused CSR kernel's nest): rows (loop 0) dynamic(rows_chunk)
     over ALL warps of the GPU (cluster..warp collapsed: flags = intersection,
     dynamic and atomic hold); the block's nonzeros (loop 2 = the collapsed
-    (row, nonzero) space) static(8) over the lanes.  Rows longer than
-    1024 nonzeros are re-bound by length class to dynamic(8192) segments over
+    (row, nonzero) space) static(lane_chunk) over the lanes (8 or 16).  Rows longer than
+    4096 nonzeros are re-bound by length class to dynamic(8192) segments over
     the warps (kernel_segmented.cu; reading #14)."""
     lv = []
     if with_gpu:
         lv.append(Level(HPAR_GPU, HPAR_GPU, STATIC, loop=0))
     lv += [Level(HPAR_CLUSTER, HPAR_WARP, DYNAMIC, loop=0, chunk=rows_chunk),
-           Level(HPAR_LANE, HPAR_LANE, STATIC_CHUNK, loop=2, chunk=8)]
+           Level(HPAR_LANE, HPAR_LANE, STATIC_CHUNK, loop=2, chunk=lane_chunk)]
     return lv
 
 

@@ -1,4 +1,4 @@
-# usage: bash scripts/profile_one.sh <config> <kernel-regex> [extra bench args]
+# usage: bash scripts/profile_one.sh <config> <kernel-regex> [extra bench args]   (env knobs pass through)
 mkdir -p gpurun_out
 c=$1; k=$2; shift 2
 CMD="python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline $*"

@@ -330,7 +330,7 @@ def _csr_cases():
     yield "zipf", off_z
     yield "all_empty", np.zeros(501, dtype=np.int64)
     yield "one_huge_row", np.array([0, (1 << 20) + 3], dtype=np.int64)
-    lens = np.array([0, 1, 0, 0, 1024, 1025, 0, 3, 2048 + 5, 0, 0, 127, 128, 129, 0, 8192, 8193, 1, 0],
+    lens = np.array([0, 1, 0, 0, 1024, 1025, 0, 3, 2048 + 5, 0, 0, 127, 128, 129, 0, 4096, 4097, 0, 8192, 8193, 1, 0],
                     dtype=np.int64)
     lens = np.tile(lens, 20)
     off = np.zeros(lens.size + 1, dtype=np.int64)
@@ -369,7 +369,7 @@ def test_segmented_csr_kernel(H, torch_mod, oracle, case):
         lens = np.diff(off)
         rb = nests.c3_fast_nest()[1].chunk
         for b0 in range(0, rows, rb):
-            rs = [r for r in range(b0, min(b0 + rb, rows)) if 0 < lens[r] <= 1024]
+            rs = [r for r in range(b0, min(b0 + rb, rows)) if 0 < lens[r] <= 4096]
             if rs:
                 ws_ = np.concatenate([own[off[r]:off[r + 1]] for r in rs])
                 assert (ws_ == ws_[0]).all(), "a block's short rows span several warps"
