@@ -309,6 +309,86 @@ hpar_status hpar_nest_resolve(const hpar_sync_construct* constructs, int32_t n, 
  * level names.  Writes the hardware range of `name`. */
 hpar_status hpar_level_alias(const char* name, int32_t* first, int32_t* last);
 
+/* ---- hierarchical memory: ghost maps (§4) --
+ * A construct at one level maps one array section per sibling d:
+ *   map(to(d):   A[off_r : len_r][off_c : len_c])   what d holds, ghosts incl.
+ *   map(from(d): A[off_r : len_r][off_c : len_c])   what d writes back
+ * per dimension offset = mul * coord + add, coord = (d / grid_cols,
+ * d % grid_cols) — the paper's `(d/2)*511 : 513` form; sections are
+ * offset:length (OpenMP array sections).  The to-sections may overlap (the
+ * ghost surface); the from-sections "must have unique sources"
+ * (P:383).  All host-side and pure (no device work). */
+typedef struct {
+  int64_t mul, add, len;
+} hpar_map_dim;
+typedef struct {
+  int64_t extent[2];     /* parent array rows, cols                       */
+  int32_t siblings;      /* S                                              */
+  int32_t grid_cols;     /* sibling grid width (coords of d above)         */
+  hpar_map_dim to[2];    /* rows, cols                                     */
+  hpar_map_dim from[2];  /* rows, cols                                     */
+} hpar_map_spec;
+typedef struct {
+  int64_t off[2]; /* first row, first col (global coordinates) */
+  int64_t len[2]; /* rows, cols                                */
+} hpar_rect;
+
+/* Sections of sibling d (0 <= d < siblings), else HPAR_E_INVALID. */
+hpar_status hpar_map_sections(const hpar_map_spec* m, int32_t d, hpar_rect* to, hpar_rect* from);
+
+/* positive lengths; every section inside the array; from(d)
+ * inside to(d); from-sections pairwise disjoint.  Returns HPAR_E_INVALID on
+ * the first violation; for an overlap, `where` (if non-NULL) receives
+ * {row, col, sibling_a, sibling_b} of the first shared element in row-major
+ * order (a < b).  O(S^2) rectangle tests, no per-element work. */
+hpar_status hpar_map_validate(const hpar_map_spec* m, int64_t where[4]);
+
+/* Halo exchange list of sibling d (device-level ghost refresh): for every
+ * other sibling e in ascending order, first the rectangle to(d) ∩ from(e)
+ * that d receives from e (send = 0), then to(e) ∩ from(d) that d sends to e
+ * (send = 1); empty intersections are omitted.  Writes min(cap, total)
+ * entries to `out` (may be NULL when cap = 0) and the total to *n. */
+typedef struct {
+  int32_t peer;
+  int32_t send;
+  hpar_rect rect; /* global coordinates */
+} hpar_halo;
+hpar_status hpar_map_exchange_plan(const hpar_map_spec* m, int32_t d, hpar_halo* out, int32_t cap, int32_t* n);
+
+/* One 5-point stencil step inside a sibling's packed buffer (§4's stencil
+ * workload).  Every cell of `from` becomes
+ *   ((((c + north) + south) + west) + east) / 5      (fp32, in that order)
+ * except cells on the parent array's boundary (row 0 / extent[0]-1, col 0 /
+ * extent[1]-1), which copy through.  Reads `in`, writes `out`; both hold the
+ * to-section row-major (to.len[0] rows, pitch `ld` floats, ld >= to.len[1],
+ * ld % 4 == 0, 16-byte aligned) on the nest's device; cells of `out` outside
+ * `from` are not written.  The kernel tiles `from` over the CTAs (static,
+ * persistent); a CTA's tile arrives by a 2-D TMA box with a 1-cell ghost
+ * ring — the same map one level down (block-shared memory).
+ * Errors: HPAR_E_INVALID (from ⊄ to, a non-boundary from cell whose
+ * neighbour lies outside to, layout/alignment), HPAR_E_CUDA. */
+typedef struct {
+  const float* in;
+  float* out;
+  int64_t ld;
+  hpar_rect to;
+  hpar_rect from;
+  int64_t extent[2];
+} hpar_stencil_desc;
+hpar_status hpar_stencil5(hpar_nest_t nest, const hpar_stencil_desc* desc, void* stream);
+
+/* Ghost refresh at the device level over the nest's NCCL communicator
+ * (rank = sibling; needs siblings == nranks): every rectangle of this
+ * rank's exchange plan goes through a packed staging buffer with
+ * ncclSend/ncclRecv in one NCCL group on `stream`.  One rank: no-op.
+ * `buf` = this rank's to-section buffer (pitch ld floats). */
+hpar_status hpar_map_exchange(hpar_nest_t nest, const hpar_map_spec* m, float* buf, int64_t ld, void* stream);
+
+/* The same refresh among S sibling buffers on ONE device (tests, replicas):
+ * bufs[d] = sibling d's to-section buffer (pitch ld floats); 2-D
+ * device-to-device copies on `stream`. */
+hpar_status hpar_map_exchange_local(const hpar_map_spec* m, float* const* bufs, int64_t ld, void* stream);
+
 /* Thread-local text of the last error ("" if none). */
 const char* hpar_last_error(void);
 /* Name of the kernel specialisation the last hpar_parallel_for_reduce on

@@ -1,0 +1,191 @@
+// kernel_stencil.cu — one 5-point Jacobi step inside a sibling's packed
+// buffer (the §4 ghost-map workload).
+//
+// Levels: the device level's map (hpar_map_*: each GPU holds its
+// to-section, ghost surface included, and writes back its from-section) is
+// host-side; this kernel is everything below it:
+//   CTA   static(1) over the 2-D tiles of the from-section (persistent grid,
+//         round robin).  Each tile arrives as ONE 2-D TMA box with a 1-cell
+//         ghost ring — the §4 map one level down ("supporting the map
+//         clause for lower-level memories such as block-shared memory"):
+//         to = tile + ghosts (rows -1..TY, cols -4..TX+3 for 16-byte
+//         alignment), from = the tile.  Cells outside the to-section buffer
+//         are zero-filled by the TMA unit (never used: they lie beyond the
+//         parent array's boundary, where cells copy through).
+//   warp  static over tile rows (4 per warp)
+//   lane  static(4) over tile columns (one float4 per lane and row)
+// Arithmetic (exact parity with oracle/ghostmap.py): each interior cell is
+// ((((c + n) + s) + w) + e) / 5 in IEEE fp32 (__fadd_rn / __fdiv_rn, no
+// contraction); parent-boundary cells copy.  2-stage TMA ring per CTA: the
+// next tile's box is in flight while this one is computed.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hpar.h"
+#include "level_primitives.cuh"
+
+namespace hpar {
+namespace {
+
+constexpr int TY = 32, TX = 128;         // outputs per CTA tile
+constexpr int BY = TY + 2, BX = TX + 8;  // TMA box (rows, cols)
+constexpr int STAGE = ((BY * BX * 4 + 127) / 128) * 128;  // bytes per ring stage (128-byte aligned)
+constexpr int NST = 2;
+constexpr int THREADS = 256;  // 8 warps x 4 rows = TY; 32 lanes x 4 cols = TX
+
+struct StParams {
+  float* out;
+  int64_t ld;
+  int fr0, fc0;       // from-section origin, local coordinates
+  int nrows, ncols;   // from-section extent
+  int ca0;            // tiling column origin (fc0 rounded down to 4)
+  int tiles_x, ntiles;
+  int64_t gr0, gc0;   // global coordinates of local (0, 0) = to.off
+  int64_t R, C;       // parent extents
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_addr(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ float avg5(float c, float n, float s, float w, float e) {
+  return __fdiv_rn(__fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(c, n), s), w), e), 5.0f);
+}
+
+__global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                            const StParams p) {
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  __shared__ uint64_t bar[NST];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
+    fence_mbarrier_init_cluster();
+  }
+  __syncthreads();
+  auto issue = [&](int t, int s) {
+    const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
+    mbar_arrive_expect_tx(&bar[s], (uint32_t)(BY * BX * 4));
+    tma_load_2d(st_smem + s * STAGE, &tmap, p.ca0 + tx * TX - 4, p.fr0 + ty * TY - 1, &bar[s]);
+  };
+  int it = 0;
+  if (tid == 0 && (int)blockIdx.x < p.ntiles) issue(blockIdx.x, 0);
+  const bool vec_ok = (p.ld & 3) == 0;
+  for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+    const int s = it & 1;
+    // the other stage was released by the barrier that ended the previous tile
+    if (tid == 0 && t + (int)gridDim.x < p.ntiles) issue(t + gridDim.x, s ^ 1);
+    mbar_wait(&bar[s], (unsigned)((it >> 1) & 1));
+    const float* S = (const float*)(st_smem + s * STAGE);
+    const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
+    const int y0 = p.fr0 + ty * TY, xb = p.ca0 + tx * TX;  // local coordinates of the tile's (0, 0)
+    const int col = 4 * lane;
+    const int64_t gx0 = p.gc0 + xb + col;  // global column of this lane's first cell
+    bool colb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) colb[i] = (gx0 + i == 0) || (gx0 + i == p.C - 1);
+    const int lx = xb + col;  // local column of this lane's first cell
+    const bool cols_full = lx >= p.fc0 && lx + 4 <= p.fc0 + p.ncols;
+    float4 nr = *(const float4*)(S + (4 * warp) * BX + col + 4);
+    float4 cr = *(const float4*)(S + (4 * warp + 1) * BX + col + 4);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = 4 * warp + k;  // tile row; smem row r + 1
+      const float4 sr = *(const float4*)(S + (r + 2) * BX + col + 4);
+      float left = __shfl_up_sync(0xffffffffu, cr.w, 1);
+      float right = __shfl_down_sync(0xffffffffu, cr.x, 1);
+      if (lane == 0) left = S[(r + 1) * BX + 3];
+      if (lane == 31) right = S[(r + 1) * BX + 4 + TX];
+      const int ly = y0 + r;
+      const int64_t gy = p.gr0 + ly;
+      const bool rowb = (gy == 0) || (gy == p.R - 1);
+      float4 o;
+      o.x = (rowb || colb[0]) ? cr.x : avg5(cr.x, nr.x, sr.x, left, cr.y);
+      o.y = (rowb || colb[1]) ? cr.y : avg5(cr.y, nr.y, sr.y, cr.x, cr.z);
+      o.z = (rowb || colb[2]) ? cr.z : avg5(cr.z, nr.z, sr.z, cr.y, cr.w);
+      o.w = (rowb || colb[3]) ? cr.w : avg5(cr.w, nr.w, sr.w, cr.z, right);
+      if (ly < p.fr0 + p.nrows) {
+        float* dst = p.out + (int64_t)ly * p.ld + lx;
+        if (cols_full && vec_ok) {
+          __stcs((float4*)dst, o);
+        } else {
+          const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (lx + i >= p.fc0 && lx + i < p.fc0 + p.ncols) dst[i] = ov[i];
+        }
+      }
+      nr = cr;
+      cr = sr;
+    }
+    __syncthreads();  // stage s is free again
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }
+  return fn;
+}
+
+}  // namespace
+
+cudaError_t launch_stencil5(const hpar_stencil_desc& d, int device, int sm_count, cudaStream_t s, const char** why) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+  if (!enc) {
+    *why = "cuTensorMapEncodeTiled unavailable";
+    return cudaErrorNotSupported;
+  }
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)d.to.len[1], (cuuint64_t)d.to.len[0]};
+  const cuuint64_t strides[1] = {(cuuint64_t)d.ld * 4};
+  const cuuint32_t box[2] = {BX, BY};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)d.in, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    *why = "cuTensorMapEncodeTiled rejected the buffer layout";
+    return cudaErrorInvalidValue;
+  }
+  StParams p;
+  p.out = d.out;
+  p.ld = d.ld;
+  p.fr0 = (int)(d.from.off[0] - d.to.off[0]);
+  p.fc0 = (int)(d.from.off[1] - d.to.off[1]);
+  p.nrows = (int)d.from.len[0];
+  p.ncols = (int)d.from.len[1];
+  p.ca0 = p.fc0 & ~3;
+  p.tiles_x = (p.fc0 + p.ncols - p.ca0 + TX - 1) / TX;
+  const int tiles_y = (p.nrows + TY - 1) / TY;
+  p.ntiles = p.tiles_x * tiles_y;
+  p.gr0 = d.to.off[0];
+  p.gc0 = d.to.off[1];
+  p.R = d.extent[0];
+  p.C = d.extent[1];
+  const int smem = NST * STAGE;
+  cudaError_t e = cudaFuncSetAttribute(stencil5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stencil5_kernel, THREADS, smem);
+  if (e != cudaSuccess) return e;
+  (void)device;
+  int grid = sm_count * (per_sm > 0 ? per_sm : 1);
+  if (grid > p.ntiles) grid = p.ntiles;
+  if (grid < 1) return cudaSuccess;
+  stencil5_kernel<<<grid, THREADS, smem, s>>>(map, p);
+  return cudaGetLastError();
+}
+
+}  // namespace hpar

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "hpar.h"
 #include "nccl.h"  // types only; functions are resolved with dlsym
@@ -40,6 +41,8 @@ void segmented_ws_qrow(int64_t nnz, size_t* off, size_t* len);
 cudaError_t launch_affine_rank_fold(const void* gathered, int G, void* out, cudaStream_t s);
 bool teams_matches(const NestArgs& a, const char** why);
 cudaError_t launch_teams(const NestArgs& a, int W, cudaStream_t s, const char** name);
+// kernel_stencil.cu
+cudaError_t launch_stencil5(const hpar_stencil_desc& d, int device, int sm_count, cudaStream_t s, const char** why);
 }  // namespace hpar
 
 using namespace hpar;
@@ -81,6 +84,10 @@ struct NcclApi {
   ncclResult_t (*commUserRank)(const ncclComm_t, int*) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
   const char* (*getLastError)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
 };
 NcclApi g_nccl;
 std::once_flag g_nccl_once;
@@ -100,6 +107,10 @@ void load_nccl() {
   g_nccl.commUserRank = (decltype(g_nccl.commUserRank))dlsym(h, "ncclCommUserRank");
   g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
   g_nccl.getLastError = (decltype(g_nccl.getLastError))dlsym(h, "ncclGetLastError");
+  g_nccl.send = (decltype(g_nccl.send))dlsym(h, "ncclSend");
+  g_nccl.recv = (decltype(g_nccl.recv))dlsym(h, "ncclRecv");
+  g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
   g_nccl.loaded = g_nccl.allReduce && g_nccl.commCount && g_nccl.commUserRank && g_nccl.getErrorString;
   if (!g_nccl.loaded) g_nccl.why = "libnccl.so.2 lacks required symbols";
 }
@@ -259,6 +270,8 @@ struct hpar_nest {
   void* gather_buf = nullptr;  // node level of ordered ops: G gathered results
   void* seg_ws = nullptr;  // CSR segmented kernel workspace (grown on demand)
   size_t seg_ws_bytes = 0;
+  float* halo_buf = nullptr;  // ghost exchange staging (grown on demand)
+  size_t halo_bytes = 0;
 };
 
 namespace {
@@ -491,6 +504,7 @@ extern "C" hpar_status hpar_nest_destroy(hpar_nest_t n) {
     cudaFree(n->barrier_word);
     cudaFree(n->seg_ws);
     cudaFree(n->gather_buf);
+    cudaFree(n->halo_buf);
   }
   delete n;
   return ok();
@@ -906,4 +920,229 @@ extern "C" hpar_status hpar_level_alias(const char* name, int32_t* first, int32_
       return ok();
     }
   return fail(HPAR_E_INVALID, "unknown level or alias '%s'", name);
+}
+
+// ------------------------------------------- ghost maps (§4; NEXT f3) ----
+namespace {
+bool rect_empty(const hpar_rect& r) { return r.len[0] <= 0 || r.len[1] <= 0; }
+hpar_rect rect_and(const hpar_rect& a, const hpar_rect& b) {
+  hpar_rect r;
+  for (int k = 0; k < 2; ++k) {
+    const int64_t lo = std::max(a.off[k], b.off[k]);
+    const int64_t hi = std::min(a.off[k] + a.len[k], b.off[k] + b.len[k]);
+    r.off[k] = lo;
+    r.len[k] = hi > lo ? hi - lo : 0;
+  }
+  return r;
+}
+bool rect_inside(const hpar_rect& in, const hpar_rect& out) {
+  for (int k = 0; k < 2; ++k)
+    if (in.off[k] < out.off[k] || in.off[k] + in.len[k] > out.off[k] + out.len[k]) return false;
+  return true;
+}
+// offset = mul * coord + add, coord = (d / grid_cols, d % grid_cols)
+void sections_of(const hpar_map_spec* m, int32_t d, hpar_rect* to, hpar_rect* from) {
+  const int64_t coord[2] = {d / m->grid_cols, d % m->grid_cols};
+  for (int k = 0; k < 2; ++k) {
+    to->off[k] = m->to[k].mul * coord[k] + m->to[k].add;
+    to->len[k] = m->to[k].len;
+    from->off[k] = m->from[k].mul * coord[k] + m->from[k].add;
+    from->len[k] = m->from[k].len;
+  }
+}
+hpar_status spec_ok(const hpar_map_spec* m) {
+  if (!m) return fail(HPAR_E_INVALID, "map spec is NULL");
+  if (m->siblings < 1 || m->grid_cols < 1) return fail(HPAR_E_INVALID, "map: siblings and grid_cols must be >= 1");
+  if (m->extent[0] < 1 || m->extent[1] < 1) return fail(HPAR_E_INVALID, "map: empty parent array");
+  return HPAR_OK;
+}
+}  // namespace
+
+extern "C" hpar_status hpar_map_sections(const hpar_map_spec* m, int32_t d, hpar_rect* to, hpar_rect* from) {
+  if (hpar_status st = spec_ok(m)) return st;
+  if (d < 0 || d >= m->siblings || !to || !from) return fail(HPAR_E_INVALID, "map: sibling %d out of range", d);
+  sections_of(m, d, to, from);
+  return ok();
+}
+
+extern "C" hpar_status hpar_map_validate(const hpar_map_spec* m, int64_t where[4]) {
+  if (hpar_status st = spec_ok(m)) return st;
+  const hpar_rect whole = {{0, 0}, {m->extent[0], m->extent[1]}};
+  for (int32_t d = 0; d < m->siblings; ++d) {
+    hpar_rect to, fr;
+    sections_of(m, d, &to, &fr);
+    if (rect_empty(to) || rect_empty(fr)) return fail(HPAR_E_INVALID, "map: sibling %d has a non-positive length", d);
+    if (!rect_inside(to, whole)) return fail(HPAR_E_INVALID, "map: sibling %d to-section outside the array", d);
+    if (!rect_inside(fr, whole)) return fail(HPAR_E_INVALID, "map: sibling %d from-section outside the array", d);
+    if (!rect_inside(fr, to)) return fail(HPAR_E_INVALID, "map: sibling %d from-section not inside its to-section", d);
+  }
+  // the first shared element in row-major order (ties: lowest pair)
+  bool found = false;
+  int64_t best[4] = {0, 0, 0, 0};
+  for (int32_t a = 0; a < m->siblings; ++a) {
+    hpar_rect ta, fa;
+    sections_of(m, a, &ta, &fa);
+    for (int32_t b = a + 1; b < m->siblings; ++b) {
+      hpar_rect tb, fb;
+      sections_of(m, b, &tb, &fb);
+      const hpar_rect x = rect_and(fa, fb);
+      if (rect_empty(x)) continue;
+      const int64_t cand[4] = {x.off[0], x.off[1], a, b};
+      if (!found || std::lexicographical_compare(cand, cand + 4, best, best + 4)) {
+        std::copy(cand, cand + 4, best);
+        found = true;
+      }
+    }
+  }
+  if (found) {
+    if (where) std::copy(best, best + 4, where);
+    return fail(HPAR_E_INVALID, "map: element (%lld, %lld) is written back by siblings %lld and %lld (P:383)",
+                (long long)best[0], (long long)best[1], (long long)best[2], (long long)best[3]);
+  }
+  return ok();
+}
+
+extern "C" hpar_status hpar_map_exchange_plan(const hpar_map_spec* m, int32_t d, hpar_halo* out, int32_t cap,
+                                              int32_t* n) {
+  if (hpar_status st = spec_ok(m)) return st;
+  if (d < 0 || d >= m->siblings || !n || (cap > 0 && !out)) return fail(HPAR_E_INVALID, "map plan: bad arguments");
+  hpar_rect tod, frd;
+  sections_of(m, d, &tod, &frd);
+  int32_t k = 0;
+  for (int32_t e = 0; e < m->siblings; ++e) {
+    if (e == d) continue;
+    hpar_rect toe, fre;
+    sections_of(m, e, &toe, &fre);
+    const hpar_rect rr[2] = {rect_and(tod, fre), rect_and(toe, frd)};
+    for (int s = 0; s < 2; ++s) {
+      if (rect_empty(rr[s])) continue;
+      if (k < cap) out[k] = hpar_halo{e, s, rr[s]};
+      ++k;
+    }
+  }
+  *n = k;
+  return ok();
+}
+
+namespace {
+hpar_status check_stencil(const hpar_stencil_desc* d) {
+  if (!d || !d->in || !d->out) return fail(HPAR_E_INVALID, "stencil: NULL descriptor or buffer");
+  if (rect_empty(d->to) || rect_empty(d->from)) return fail(HPAR_E_INVALID, "stencil: empty section");
+  if (!rect_inside(d->from, d->to)) return fail(HPAR_E_INVALID, "stencil: from-section not inside the to-section");
+  const hpar_rect whole = {{0, 0}, {d->extent[0], d->extent[1]}};
+  if (!rect_inside(d->to, whole)) return fail(HPAR_E_INVALID, "stencil: to-section outside the array");
+  if (d->ld < d->to.len[1] || d->ld % 4 != 0)
+    return fail(HPAR_E_INVALID, "stencil: ld must be >= the to-section's columns and a multiple of 4");
+  if (((uintptr_t)d->in & 15) || ((uintptr_t)d->out & 15))
+    return fail(HPAR_E_INVALID, "stencil: buffers must be 16-byte aligned");
+  if (d->in == d->out) return fail(HPAR_E_INVALID, "stencil: in and out must differ (Jacobi step)");
+  // every non-boundary from cell needs its 4 neighbours inside `to`
+  for (int k = 0; k < 2; ++k) {
+    const int64_t lo = d->from.off[k], hi = d->from.off[k] + d->from.len[k] - 1;
+    if (lo > 0 && lo - 1 < d->to.off[k])
+      return fail(HPAR_E_INVALID, "stencil: ghost %s %lld not in the to-section", k ? "col" : "row", (long long)(lo - 1));
+    if (hi < d->extent[k] - 1 && hi + 1 >= d->to.off[k] + d->to.len[k])
+      return fail(HPAR_E_INVALID, "stencil: ghost %s %lld not in the to-section", k ? "col" : "row", (long long)(hi + 1));
+  }
+  return HPAR_OK;
+}
+// 2-D copy of global rectangle r between two buffers holding sections dto / sto
+cudaError_t copy_rect(float* dst, int64_t dld, const hpar_rect& dto, const float* src, int64_t sld,
+                      const hpar_rect& sto, const hpar_rect& r, cudaStream_t s) {
+  float* dp = dst + (r.off[0] - dto.off[0]) * dld + (r.off[1] - dto.off[1]);
+  const float* sp = src + (r.off[0] - sto.off[0]) * sld + (r.off[1] - sto.off[1]);
+  return cudaMemcpy2DAsync(dp, (size_t)dld * 4, sp, (size_t)sld * 4, (size_t)r.len[1] * 4, (size_t)r.len[0],
+                           cudaMemcpyDeviceToDevice, s);
+}
+}  // namespace
+
+extern "C" hpar_status hpar_stencil5(hpar_nest_t n, const hpar_stencil_desc* d, void* stream_) {
+  if (!n) return fail(HPAR_E_INVALID, "stencil: nest is NULL");
+  if (hpar_status st = check_stencil(d)) return st;
+  CUDA_TRY(cudaSetDevice(n->device));
+  int sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, n->device));
+  const char* why = "";
+  const cudaError_t e = launch_stencil5(*d, n->device, sms, (cudaStream_t)stream_, &why);
+  if (e != cudaSuccess) return fail(HPAR_E_CUDA, "stencil5: %s (%s)", cudaGetErrorString(e), why);
+  n->last_kernel = "stencil5_tma";
+  return ok();
+}
+
+extern "C" hpar_status hpar_map_exchange_local(const hpar_map_spec* m, float* const* bufs, int64_t ld, void* stream_) {
+  if (hpar_status st = spec_ok(m)) return st;
+  if (!bufs || ld < m->to[1].len) return fail(HPAR_E_INVALID, "map exchange: bad buffers or pitch");
+  const cudaStream_t s = (cudaStream_t)stream_;
+  for (int32_t d = 0; d < m->siblings; ++d) {
+    hpar_rect tod, frd;
+    sections_of(m, d, &tod, &frd);
+    for (int32_t e = 0; e < m->siblings; ++e) {
+      if (e == d) continue;
+      hpar_rect toe, fre;
+      sections_of(m, e, &toe, &fre);
+      const hpar_rect r = rect_and(tod, fre);
+      if (rect_empty(r)) continue;
+      CUDA_TRY(copy_rect(bufs[d], ld, tod, bufs[e], ld, toe, r, s));
+    }
+  }
+  return ok();
+}
+
+extern "C" hpar_status hpar_map_exchange(hpar_nest_t n, const hpar_map_spec* m, float* buf, int64_t ld,
+                                         void* stream_) {
+  if (!n) return fail(HPAR_E_INVALID, "map exchange: nest is NULL");
+  if (hpar_status st = spec_ok(m)) return st;
+  if (m->siblings != n->nranks)
+    return fail(HPAR_E_INVALID, "map exchange: %d siblings but %d ranks", m->siblings, n->nranks);
+  if (n->nranks == 1) return ok();
+  if (!buf || ld < m->to[1].len) return fail(HPAR_E_INVALID, "map exchange: bad buffer or pitch");
+  if (hpar_status st = need_nccl()) return st;
+  if (!g_nccl.send || !g_nccl.recv || !g_nccl.groupStart || !g_nccl.groupEnd)
+    return fail(HPAR_E_NCCL, "NCCL lacks send/recv");
+  const cudaStream_t s = (cudaStream_t)stream_;
+  const int32_t d = n->rank;
+  int32_t cnt = 0;
+  if (hpar_status st = hpar_map_exchange_plan(m, d, nullptr, 0, &cnt)) return st;
+  std::vector<hpar_halo> plan(cnt);
+  if (hpar_status st = hpar_map_exchange_plan(m, d, plan.data(), cnt, &cnt)) return st;
+  size_t total = 0;
+  for (const hpar_halo& h : plan) total += (size_t)h.rect.len[0] * h.rect.len[1];
+  CUDA_TRY(cudaSetDevice(n->device));
+  if (total * 4 > n->halo_bytes) {
+    cudaFree(n->halo_buf);
+    n->halo_buf = nullptr;
+    n->halo_bytes = 0;
+    CUDA_TRY(cudaMalloc(&n->halo_buf, total * 4));
+    n->halo_bytes = total * 4;
+  }
+  hpar_rect tod, frd;
+  sections_of(m, d, &tod, &frd);
+  std::vector<size_t> pos(cnt);
+  size_t at = 0;
+  for (int32_t i = 0; i < cnt; ++i) {  // pack the sends (staging is rect-shaped)
+    pos[i] = at;
+    const hpar_rect& r = plan[i].rect;
+    if (plan[i].send) CUDA_TRY(copy_rect(n->halo_buf + at, r.len[1], r, buf, ld, tod, r, s));
+    at += (size_t)r.len[0] * r.len[1];
+  }
+  ncclComm_t comm = (ncclComm_t)n->comm;
+  ncclResult_t r = g_nccl.groupStart();
+  if (r != ncclSuccess) return nccl_fail(r, comm, "ncclGroupStart");
+  for (int32_t i = 0; i < cnt; ++i) {
+    const size_t elems = (size_t)plan[i].rect.len[0] * plan[i].rect.len[1];
+    r = plan[i].send ? g_nccl.send(n->halo_buf + pos[i], elems, ncclFloat32, plan[i].peer, comm, s)
+                     : g_nccl.recv(n->halo_buf + pos[i], elems, ncclFloat32, plan[i].peer, comm, s);
+    if (r != ncclSuccess) {
+      g_nccl.groupEnd();
+      return nccl_fail(r, comm, plan[i].send ? "ncclSend" : "ncclRecv");
+    }
+  }
+  r = g_nccl.groupEnd();
+  if (r != ncclSuccess) return nccl_fail(r, comm, "ncclGroupEnd");
+  for (int32_t i = 0; i < cnt; ++i) {  // unpack the receives
+    if (plan[i].send) continue;
+    const hpar_rect& rr = plan[i].rect;
+    CUDA_TRY(copy_rect(buf, ld, tod, n->halo_buf + pos[i], rr.len[1], rr, rr, s));
+  }
+  return ok();
 }

@@ -103,6 +103,31 @@ class ReduceDesc(ctypes.Structure):
                 ("fingerprint", ctypes.c_void_p), ("global_begin", ctypes.c_uint64)]
 
 
+class MapDim(ctypes.Structure):
+    _fields_ = [("mul", ctypes.c_int64), ("add", ctypes.c_int64), ("len", ctypes.c_int64)]
+
+
+class MapSpec(ctypes.Structure):
+    _fields_ = [("extent", ctypes.c_int64 * 2), ("siblings", ctypes.c_int32), ("grid_cols", ctypes.c_int32),
+                ("to", MapDim * 2), ("from_", MapDim * 2)]
+
+
+class Rect(ctypes.Structure):
+    _fields_ = [("off", ctypes.c_int64 * 2), ("len", ctypes.c_int64 * 2)]
+
+    def tup(self) -> tuple:
+        return (self.off[0], self.off[1], self.len[0], self.len[1])
+
+
+class Halo(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int32), ("send", ctypes.c_int32), ("rect", Rect)]
+
+
+class StencilDesc(ctypes.Structure):
+    _fields_ = [("in_", ctypes.c_void_p), ("out", ctypes.c_void_p), ("ld", ctypes.c_int64), ("to", Rect),
+                ("from_", Rect), ("extent", ctypes.c_int64 * 2)]
+
+
 # ---- library --------------------------------------------------------------
 _lib = None
 
@@ -130,6 +155,15 @@ def lib() -> ctypes.CDLL:
             "hpar_nest_resolve": [ctypes.POINTER(SyncConstruct), ctypes.c_int32, ctypes.POINTER(LevelInfo),
                                   ctypes.POINTER(NestLevel)],
             "hpar_level_alias": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
+            "hpar_map_sections": [ctypes.POINTER(MapSpec), ctypes.c_int32, ctypes.POINTER(Rect), ctypes.POINTER(Rect)],
+            "hpar_map_validate": [ctypes.POINTER(MapSpec), ctypes.POINTER(ctypes.c_int64)],
+            "hpar_map_exchange_plan": [ctypes.POINTER(MapSpec), ctypes.c_int32, ctypes.POINTER(Halo), ctypes.c_int32,
+                                       ctypes.POINTER(ctypes.c_int32)],
+            "hpar_stencil5": [ctypes.c_void_p, ctypes.POINTER(StencilDesc), ctypes.c_void_p],
+            "hpar_map_exchange": [ctypes.c_void_p, ctypes.POINTER(MapSpec), ctypes.c_void_p, ctypes.c_int64,
+                                  ctypes.c_void_p],
+            "hpar_map_exchange_local": [ctypes.POINTER(MapSpec), ctypes.POINTER(ctypes.c_void_p), ctypes.c_int64,
+                                        ctypes.c_void_p],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -314,3 +348,62 @@ def make_desc(x, out, *, op: int = OP_SUM, n0: int, n1: int = 0, ld: int = 0, nl
     d.fingerprint = fingerprint.data_ptr() if fingerprint is not None else None
     d.global_begin = global_begin
     return d
+
+
+# ---- hierarchical memory: ghost maps + stencil (§4; NEXT f3) -----------------
+def map_spec(extent, siblings: int, grid_cols: int, to, frm) -> MapSpec:
+    """to / frm: ((mul, add, len) rows, (mul, add, len) cols) — P:376-377."""
+    m = MapSpec()
+    m.extent[0], m.extent[1] = extent
+    m.siblings, m.grid_cols = siblings, grid_cols
+    for k in range(2):
+        m.to[k] = MapDim(*to[k])
+        m.from_[k] = MapDim(*frm[k])
+    return m
+
+
+def hpar_map_sections(m: MapSpec, d: int) -> tuple[Rect, Rect]:
+    to, fr = Rect(), Rect()
+    _check(lib().hpar_map_sections(ctypes.byref(m), d, ctypes.byref(to), ctypes.byref(fr)))
+    return to, fr
+
+
+def hpar_map_validate(m: MapSpec):
+    """None if valid; raises HparError (with .where = (row, col, a, b) on an overlap)."""
+    w = (ctypes.c_int64 * 4)(-1, -1, -1, -1)
+    rc = lib().hpar_map_validate(ctypes.byref(m), w)
+    if rc != HPAR_OK:
+        e = HparError(rc, lib().hpar_last_error().decode())
+        e.where = tuple(w) if w[0] >= 0 else None
+        raise e
+
+
+def hpar_map_exchange_plan(m: MapSpec, d: int) -> list[tuple]:
+    """[(peer, 'recv'|'send', (r0, c0, rows, cols))] in plan order."""
+    n = ctypes.c_int32(0)
+    _check(lib().hpar_map_exchange_plan(ctypes.byref(m), d, None, 0, ctypes.byref(n)))
+    arr = (Halo * max(n.value, 1))()
+    _check(lib().hpar_map_exchange_plan(ctypes.byref(m), d, arr, n.value, ctypes.byref(n)))
+    return [(h.peer, "send" if h.send else "recv", h.rect.tup()) for h in arr[:n.value]]
+
+
+def stencil_desc(inp, out, ld: int, to: Rect, frm: Rect, extent) -> StencilDesc:
+    d = StencilDesc()
+    d.in_, d.out, d.ld = inp.data_ptr(), out.data_ptr(), ld
+    d.to, d.from_ = to, frm
+    d.extent[0], d.extent[1] = extent
+    return d
+
+
+def hpar_stencil5(nest: "Nest", desc: StencilDesc, stream: int = 0) -> None:
+    _check(lib().hpar_stencil5(nest.handle, ctypes.byref(desc), ctypes.c_void_p(stream)))
+
+
+def hpar_map_exchange(nest: "Nest", m: MapSpec, buf, ld: int, stream: int = 0) -> None:
+    _check(lib().hpar_map_exchange(nest.handle, ctypes.byref(m), ctypes.c_void_p(buf.data_ptr()), ld,
+                                   ctypes.c_void_p(stream)))
+
+
+def hpar_map_exchange_local(m: MapSpec, bufs: list, ld: int, stream: int = 0) -> None:
+    arr = (ctypes.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs])
+    _check(lib().hpar_map_exchange_local(ctypes.byref(m), arr, ld, ctypes.c_void_p(stream)))

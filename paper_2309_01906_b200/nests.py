@@ -92,5 +92,19 @@ def c3_fast_nest(with_gpu: bool = True, rows_chunk: int = 256, lane_chunk: int =
     return lv
 
 
-__all__ = ["c3_fast_nest","c1_nest", "c2_nest", "c3_nest", "c4_nest", "c5_nest", "flat_nest", "TILE_F32", "TILE_U8",
+def stencil_nest(with_gpu: bool = True) -> list[Level]:
+    """The §4 stencil workload (NEXT f3): the GPU level takes one sibling's
+    map sections (hpar_map_*); below it the from-section's rows are static
+    over the CTAs' tiles and warps (4 rows each), columns static(4) over the
+    lanes (kernel_stencil.cu)."""
+    lv = []
+    if with_gpu:
+        lv.append(Level(HPAR_GPU, HPAR_GPU, STATIC, loop=0))
+    lv += [Level(HPAR_CLUSTER, HPAR_CTA, STATIC, loop=0),
+           Level(HPAR_WARP, HPAR_WARP, STATIC, loop=0),
+           Level(HPAR_LANE, HPAR_LANE, STATIC_CHUNK, loop=1, chunk=4)]
+    return lv
+
+
+__all__ = ["stencil_nest", "c3_fast_nest","c1_nest", "c2_nest", "c3_nest", "c4_nest", "c5_nest", "flat_nest", "TILE_F32", "TILE_U8",
            "NONE"]
