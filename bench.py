@@ -121,6 +121,11 @@ def config_spec(name: str, nranks: int):
                     n0=(1 << 24) * nranks,
                     scaling="weak", seed=gen.SEED_C3, dtype="f32", elems_per_rank=1 << 28,
                     bytes_per_rank=(1 << 30) + ((1 << 24) + 1) * 8 + (1 << 24) * 4)
+    if name == "c6":  # NEXT f3: §4 ghost maps + 5-point stencil, one Jacobi sweep per step
+        tile = 16384
+        return dict(workload="c6_stencil5_16384x16384_per_gpu_f32", kind="stencil", tile=tile, n0=tile * tile,
+                    scaling="weak", seed=gen.SEED_C5, dtype="f32", elems_per_rank=tile * tile,
+                    bytes_per_rank=tile * tile * 8)
     raise SystemExit(f"unknown config {name}")
 
 
@@ -165,7 +170,40 @@ def run_hpar(args):
         args.clusters = tuned[1]
     kind = spec["kind"]
     extra_inputs = []
-    if kind == "rowwise":
+    step = e2e_step = None
+    if kind == "stencil":
+        # sibling grid: gx = 2 columns once there are 2+ GPUs; each GPU's from-
+        # tile is tile x tile with a 1-cell ghost ring (P:376-377 form)
+        tile = spec["tile"]
+        gx = 1 if world == 1 else 2
+        gy = world // gx
+        extent = (gy * tile + 2, gx * tile + 2)
+        mspec = H.map_spec(extent, world, gx, [(tile, 0, tile + 2), (tile, 0, tile + 2)],
+                           [(tile, 1, tile), (tile, 1, tile)])
+        H.hpar_map_validate(mspec)
+        to, fr = H.hpar_map_sections(mspec, rank)
+        nest = H.Nest(nests.stencil_nest(), device=local, nccl_comm=comm)
+        ld = (tile + 2 + 3) // 4 * 4
+        x = torch.empty((tile + 2, ld), dtype=torch.float32, device=dev)
+        L.hpar_inputs_fill_f32(spec["seed"], rank * x.numel(), x.numel(), x.data_ptr(), sptr)
+        out = x.clone()
+        descs = [H.stencil_desc(x, out, ld, to, fr, extent), H.stencil_desc(out, x, ld, to, fr, extent)]
+        bufs = [x, out]
+        phase = [0]
+
+        def step():
+            H.hpar_stencil5(nest, descs[phase[0]], sptr)
+            H.hpar_map_exchange(nest, mspec, bufs[1 - phase[0]], ld, sptr)
+            phase[0] ^= 1
+
+        def e2e_step():  # host input -> x, one sweep into out (+ ghost refresh), out -> host
+            H.hpar_stencil5(nest, descs[0], sptr)
+            H.hpar_map_exchange(nest, mspec, out, ld, sptr)
+
+        elems_rank = tile * tile
+        alg_bytes = tile * tile * 8
+        host_in_bytes, host_out_bytes = x.numel() * 4, out.numel() * 4
+    elif kind == "rowwise":
         nest = H.Nest(nests.c2_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
                       clusters=args.clusters)
         b, cnt = nest.shard_range(spec["n0"], rank)
@@ -230,8 +268,11 @@ def run_hpar(args):
         extra_inputs = [off]
     torch.cuda.synchronize()
 
-    def step():
-        nest.parallel_for_reduce(desc, sptr)
+    if step is None:
+        def step():
+            nest.parallel_for_reduce(desc, sptr)
+    if e2e_step is None:
+        e2e_step = step
 
     for _ in range(args.warmup):
         step()
@@ -285,10 +326,10 @@ def run_hpar(args):
         dev_inputs = [x] + extra_inputs
         host_inputs = []
         for t_ in dev_inputs:
-            h_ = torch.empty(t_.numel(), dtype=t_.dtype, pin_memory=True)
+            h_ = torch.empty(tuple(t_.shape), dtype=t_.dtype, pin_memory=True)
             h_.copy_(t_)
             host_inputs.append(h_)
-        host_out = torch.empty(out.numel(), dtype=out.dtype, pin_memory=True)
+        host_out = torch.empty(tuple(out.shape), dtype=out.dtype, pin_memory=True)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -298,7 +339,7 @@ def run_hpar(args):
         for _ in range(e2e_steps):
             for d_, h_ in zip(dev_inputs, host_inputs):
                 d_.copy_(h_, non_blocking=True)
-            step()
+            e2e_step()
             host_out.copy_(out, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -379,6 +420,18 @@ def cpu_baseline(config: str, budget_s: float = 10.0, samples: int = 1):
         dt = time.perf_counter() - t0
         return {"value": reps * n / dt, "unit": "elements/s", "cores": cores, "kind": "oracle",
                 "sample": f"{f.__name__} over the first 2^26 elements, {reps} passes, {dt:.1f} s"}
+    if config in ("c3", "c6"):
+        f, n, what = oracle_step_fn(config, 1 << 24)
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            f()
+            reps += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return {"value": reps * n / dt, "unit": "elements/s", "cores": cores, "kind": "oracle",
+                "sample": f"{what}, {reps} passes, {dt:.1f} s"}
     if config == "c4":
         n = 1 << 26
         x = gen.gen_u8(gen.SEED_C4, 0, n)
@@ -414,6 +467,11 @@ def oracle_step_fn(config: str, n_elems: int):
         v = gen.gen_f32(gen.SEED_C3, 0, nnz)
         o = off[: rows + 1].copy()
         return (lambda: O.segsum_f32(v, o)), nnz, f"or_segsum_f32 over rows [0,{rows}) ({nnz} nonzeros)"
+    if config == "c6":
+        from oracle import ghostmap as G
+        side = int(max(64, min(16386, int(np.sqrt(max(n_elems, 1))))))
+        a = gen.gen_f32(gen.SEED_C5, 0, side * side).reshape(side, side)
+        return (lambda: G.stencil5_step(a)), side * side, f"ghostmap.stencil5_step (numpy fp32) on {side} x {side}"
     n = max(1024, n_elems)
     if config == "c4":
         x = gen.gen_u8(gen.SEED_C4, 0, n)
@@ -465,7 +523,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
     ap.add_argument("--impl", default="hpar", choices=["hpar", "reference"])
     ap.add_argument("--clusters", type=int, default=-1, help="C (0 = resident clusters, -1 = tuned default)")
     ap.add_argument("--warps", type=int, default=0, help="W warps per CTA (0 = tuned default)")
