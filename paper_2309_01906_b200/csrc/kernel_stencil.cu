@@ -12,16 +12,20 @@
 //         alignment), from = the tile.  Cells outside the to-section buffer
 //         are zero-filled by the TMA unit (never used: they lie beyond the
 //         parent array's boundary, where cells copy through).
-//   warp  static over tile rows (4 per warp)
+//   warp  static over tile rows (TY / 8 per warp; TY = 64 by default)
 //   lane  static(4) over tile columns (one float4 per lane and row)
 // Arithmetic (exact parity with oracle/ghostmap.py): each interior cell is
-// ((((c + n) + s) + w) + e) / 5 in IEEE fp32 (__fadd_rn / __fdiv_rn, no
-// contraction); parent-boundary cells copy.  2-stage TMA ring per CTA: the
-// next tile's box is in flight while this one is computed.
+// ((((c + n) + s) + w) + e) / 5 in IEEE fp32 (__fadd_rn, and a division by
+// 5 that is correctly rounded for every input, see div5); parent-boundary
+// cells copy.  Tiles without boundary or section edges take a branch-free
+// path.  2-stage TMA ring per CTA: the next tile's box is in flight while
+// this one is computed.  Measured alternatives (scripts/sweep_stencil.sh):
+// TY = 16 / 32, 3-4 stages, L2 promotion off, per-CTA column-strip walks.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "hpar.h"
 #include "level_primitives.cuh"
@@ -29,11 +33,15 @@
 namespace hpar {
 namespace {
 
-constexpr int TY = 32, TX = 128;         // outputs per CTA tile
-constexpr int BY = TY + 2, BX = TX + 8;  // TMA box (rows, cols)
-constexpr int STAGE = ((BY * BX * 4 + 127) / 128) * 128;  // bytes per ring stage (128-byte aligned)
-constexpr int NST = 2;
-constexpr int THREADS = 256;  // 8 warps x 4 rows = TY; 32 lanes x 4 cols = TX
+constexpr int TX = 128;       // tile columns: 32 lanes x 4
+constexpr int BX = TX + 8;    // TMA box columns: 4 left (16-byte alignment of the tile) + 4 right
+constexpr int THREADS = 256;  // 8 warps, TY / 8 rows each
+template <int TY, int NST>
+struct Geo {
+  static constexpr int BY = TY + 2;                                // TMA box rows (1 ghost row each side)
+  static constexpr int STAGE = ((BY * BX * 4 + 127) / 128) * 128;  // bytes per ring stage (128-byte aligned)
+  static constexpr int RPW = TY / 8;                               // rows per warp
+};
 
 struct StParams {
   float* out;
@@ -41,7 +49,7 @@ struct StParams {
   int fr0, fc0;       // from-section origin, local coordinates
   int nrows, ncols;   // from-section extent
   int ca0;            // tiling column origin (fc0 rounded down to 4)
-  int tiles_x, ntiles;
+  int tiles_x, tiles_y, ntiles;
   int64_t gr0, gc0;   // global coordinates of local (0, 0) = to.off
   int64_t R, C;       // parent extents
 };
@@ -54,12 +62,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// a / 5 correctly rounded (== __fdiv_rn(a, 5.0f), verified for all 2^32
+// inputs by scripts/div5_exhaustive.cu): q0 = RN(a * RN(1/5)), the remainder
+// a - 5 q0 is exact by FMA, one correction step; ±0 and ±inf take q0 (the
+// only inputs where the correction differs: sign of zero, inf - inf).
+__device__ __forceinline__ float div5(float a) {
+  const float q0 = __fmul_rn(a, 0.2f);
+  const float r = __fmaf_rn(-q0, 5.0f, a);
+  const float q = __fmaf_rn(r, 0.2f, q0);
+  return (a == 0.0f || fabsf(a) == __int_as_float(0x7f800000)) ? q0 : q;
+}
 __device__ __forceinline__ float avg5(float c, float n, float s, float w, float e) {
-  return __fdiv_rn(__fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(c, n), s), w), e), 5.0f);
+  return div5(__fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(c, n), s), w), e));
 }
 
+template <int TY, int NST>
 __global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant__ CUtensorMap tmap,
                                                             const StParams p) {
+  using Gm = Geo<TY, NST>;
+  constexpr int BY = Gm::BY, STAGE = Gm::STAGE, RPW = Gm::RPW;
   extern __shared__ __align__(128) unsigned char st_smem[];
   __shared__ uint64_t bar[NST];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -68,6 +89,9 @@ __global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant
     fence_mbarrier_init_cluster();
   }
   __syncthreads();
+  // tiles in row-major order, round robin over the persistent CTAs: the tiles
+  // in flight at any time form a few contiguous row bands (sequential HBM
+  // traffic; walking column strips per CTA measured 35% slower)
   auto issue = [&](int t, int s) {
     const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
     mbar_arrive_expect_tx(&bar[s], (uint32_t)(BY * BX * 4));
@@ -76,11 +100,16 @@ __global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant
   int it = 0;
   if (tid == 0 && (int)blockIdx.x < p.ntiles) issue(blockIdx.x, 0);
   const bool vec_ok = (p.ld & 3) == 0;
+  // prologue: the first NST - 1 tiles of this CTA
+  if (tid == 0)
+    for (int j = 1; j < NST - 1; ++j)
+      if ((int)blockIdx.x + j * (int)gridDim.x < p.ntiles) issue(blockIdx.x + j * gridDim.x, j);
   for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
-    const int s = it & 1;
-    // the other stage was released by the barrier that ended the previous tile
-    if (tid == 0 && t + (int)gridDim.x < p.ntiles) issue(t + gridDim.x, s ^ 1);
-    mbar_wait(&bar[s], (unsigned)((it >> 1) & 1));
+    const int s = it % NST;
+    // the stage of tile it + NST - 1 was released by the barrier that ended tile it - 1
+    const int tn = t + (NST - 1) * (int)gridDim.x;
+    if (tid == 0 && tn < p.ntiles) issue(tn, (it + NST - 1) % NST);
+    mbar_wait(&bar[s], (unsigned)((it / NST) & 1));
     const float* S = (const float*)(st_smem + s * STAGE);
     const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
     const int y0 = p.fr0 + ty * TY, xb = p.ca0 + tx * TX;  // local coordinates of the tile's (0, 0)
@@ -91,11 +120,38 @@ __global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant
     for (int i = 0; i < 4; ++i) colb[i] = (gx0 + i == 0) || (gx0 + i == p.C - 1);
     const int lx = xb + col;  // local column of this lane's first cell
     const bool cols_full = lx >= p.fc0 && lx + 4 <= p.fc0 + p.ncols;
-    float4 nr = *(const float4*)(S + (4 * warp) * BX + col + 4);
-    float4 cr = *(const float4*)(S + (4 * warp + 1) * BX + col + 4);
+    float4 nr = *(const float4*)(S + (RPW * warp) * BX + col + 4);
+    float4 cr = *(const float4*)(S + (RPW * warp + 1) * BX + col + 4);
+    // interior tile (the common case): inside `from`, no parent-boundary cell
+    const int64_t gy0 = p.gr0 + y0, gxt = p.gc0 + xb;
+    const bool interior = vec_ok && y0 + TY <= p.fr0 + p.nrows && xb >= p.fc0 && xb + TX <= p.fc0 + p.ncols &&
+                          gy0 > 0 && gy0 + TY < p.R && gxt > 0 && gxt + TX < p.C;
+    if (interior) {
+      float* dst = p.out + (int64_t)(y0 + RPW * warp) * p.ld + lx;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int r = 4 * warp + k;  // tile row; smem row r + 1
+      for (int k = 0; k < RPW; ++k) {
+        const int r = RPW * warp + k;
+        const float4 sr = *(const float4*)(S + (r + 2) * BX + col + 4);
+        float left = __shfl_up_sync(0xffffffffu, cr.w, 1);
+        float right = __shfl_down_sync(0xffffffffu, cr.x, 1);
+        if (lane == 0) left = S[(r + 1) * BX + 3];
+        if (lane == 31) right = S[(r + 1) * BX + 4 + TX];
+        float4 o;
+        o.x = avg5(cr.x, nr.x, sr.x, left, cr.y);
+        o.y = avg5(cr.y, nr.y, sr.y, cr.x, cr.z);
+        o.z = avg5(cr.z, nr.z, sr.z, cr.y, cr.w);
+        o.w = avg5(cr.w, nr.w, sr.w, cr.z, right);
+        __stcs((float4*)dst, o);
+        dst += p.ld;
+        nr = cr;
+        cr = sr;
+      }
+      __syncthreads();  // stage s is free again
+      continue;
+    }
+#pragma unroll
+    for (int k = 0; k < RPW; ++k) {
+      const int r = RPW * warp + k;  // tile row; smem row r + 1
       const float4 sr = *(const float4*)(S + (r + 2) * BX + col + 4);
       float left = __shfl_up_sync(0xffffffffu, cr.w, 1);
       float right = __shfl_down_sync(0xffffffffu, cr.x, 1);
@@ -141,6 +197,24 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
+template <int TY, int NST>
+cudaError_t launch_ty(const CUtensorMap& map, const StParams& p0, int sm_count, cudaStream_t s) {
+  StParams p = p0;
+  p.tiles_y = (p.nrows + TY - 1) / TY;
+  p.ntiles = p.tiles_x * p.tiles_y;
+  const int smem = NST * Geo<TY, NST>::STAGE;
+  cudaError_t e = cudaFuncSetAttribute(stencil5_kernel<TY, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stencil5_kernel<TY, NST>, THREADS, smem);
+  if (e != cudaSuccess) return e;
+  int grid = sm_count * (per_sm > 0 ? per_sm : 1);
+  if (grid > p.ntiles) grid = p.ntiles;
+  if (grid < 1) return cudaSuccess;
+  stencil5_kernel<TY, NST><<<grid, THREADS, smem, s>>>(map, p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stencil5(const hpar_stencil_desc& d, int device, int sm_count, cudaStream_t s, const char** why) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
   if (!enc) {
@@ -150,11 +224,17 @@ cudaError_t launch_stencil5(const hpar_stencil_desc& d, int device, int sm_count
   CUtensorMap map;
   const cuuint64_t dims[2] = {(cuuint64_t)d.to.len[1], (cuuint64_t)d.to.len[0]};
   const cuuint64_t strides[1] = {(cuuint64_t)d.ld * 4};
-  const cuuint32_t box[2] = {BX, BY};
+  static int ty_knob = -1, l2p = -1;
+  if (ty_knob < 0) ty_knob = getenv("HPAR_ST_TY") ? atoi(getenv("HPAR_ST_TY")) : 64;
+  if (l2p < 0) l2p = getenv("HPAR_ST_L2P") ? atoi(getenv("HPAR_ST_L2P")) : 256;
+  const int TYv = (ty_knob == 64) ? 64 : (ty_knob == 16 ? 16 : 32);
+  const cuuint32_t box[2] = {BX, (cuuint32_t)(TYv + 2)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)d.in, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          l2p == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                   : (l2p == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B),
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) {
     *why = "cuTensorMapEncodeTiled rejected the buffer layout";
     return cudaErrorInvalidValue;
@@ -168,24 +248,18 @@ cudaError_t launch_stencil5(const hpar_stencil_desc& d, int device, int sm_count
   p.ncols = (int)d.from.len[1];
   p.ca0 = p.fc0 & ~3;
   p.tiles_x = (p.fc0 + p.ncols - p.ca0 + TX - 1) / TX;
-  const int tiles_y = (p.nrows + TY - 1) / TY;
-  p.ntiles = p.tiles_x * tiles_y;
   p.gr0 = d.to.off[0];
   p.gc0 = d.to.off[1];
   p.R = d.extent[0];
   p.C = d.extent[1];
-  const int smem = NST * STAGE;
-  cudaError_t e = cudaFuncSetAttribute(stencil5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stencil5_kernel, THREADS, smem);
-  if (e != cudaSuccess) return e;
   (void)device;
-  int grid = sm_count * (per_sm > 0 ? per_sm : 1);
-  if (grid > p.ntiles) grid = p.ntiles;
-  if (grid < 1) return cudaSuccess;
-  stencil5_kernel<<<grid, THREADS, smem, s>>>(map, p);
-  return cudaGetLastError();
+  static int nst_knob = -1;
+  if (nst_knob < 0) nst_knob = getenv("HPAR_ST_NST") ? atoi(getenv("HPAR_ST_NST")) : 2;
+  if (TYv == 16) return nst_knob >= 4 ? launch_ty<16, 4>(map, p, sm_count, s)
+                                      : (nst_knob == 3 ? launch_ty<16, 3>(map, p, sm_count, s) : launch_ty<16, 2>(map, p, sm_count, s));
+  if (TYv == 64) return launch_ty<64, 2>(map, p, sm_count, s);
+  return nst_knob >= 4 ? launch_ty<32, 4>(map, p, sm_count, s)
+                       : (nst_knob == 3 ? launch_ty<32, 3>(map, p, sm_count, s) : launch_ty<32, 2>(map, p, sm_count, s));
 }
 
 }  // namespace hpar

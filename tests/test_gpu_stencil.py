@@ -117,3 +117,23 @@ def test_three_by_two_siblings_with_ghost_ring(env):
                    (G.MapDim(ty, 1, ty), G.MapDim(tx, 1, tx)))
     A = field(*sp.extent, seed=gen.SEED_C4)
     assert np.array_equal(_mapped_on_one_gpu(torch, H, nest, sp, A, 3), G.stencil5(A, 3))
+
+
+def test_stencil_division_special_values(env):
+    """Every fp32 class through the kernel's division by 5 (±0, ±inf, NaN,
+    subnormals, FLT_MAX, random bit patterns): cell x sits between -0 cells,
+    so its sum is x itself and the output is x / 5, compared with numpy's
+    IEEE division via the oracle (scripts/div5_exhaustive.cu covers all 2^32
+    inputs of the same sequence)."""
+    torch, H, nest = env
+    rng = np.random.default_rng(17)
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45, 1.1754942e-38, 3.4028235e38,
+                        -3.4028235e38, 5.0, 1.0, 0.2, 1e-40, 7.0e37], dtype=np.float32)
+    vals = np.concatenate([special, rng.integers(0, 2 ** 32, 1 << 18, dtype=np.uint64).astype(np.uint32).view(np.float32)])
+    n = vals.size
+    A = np.full((3, 2 * n + 1), -0.0, dtype=np.float32)
+    A[1, 1::2] = vals
+    got = run_whole(torch, H, nest, A, 1)
+    want = G.stencil5(A, 1)
+    assert np.array_equal(got.view(np.uint32)[1, 1::2][~np.isnan(vals)], want.view(np.uint32)[1, 1::2][~np.isnan(vals)])
+    assert np.array_equal(np.isnan(got), np.isnan(want))
