@@ -1,6 +1,6 @@
 # ncu evidence for the fused kernels (run under gpurun; one GPU)
 mkdir -p gpurun_out
-for spec in "c2:rowwise" "c5:flat_tma" "c4:hist" "c3:segmented" "c1:generic"; do
+for spec in "c2:rowwise" "c5:flat_tma" "c4:hist" "c3:segmented" "c1:teams" "c6:stencil5"; do
   c=${spec%%:*}; k=${spec##*:}
   CMD="python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
   $CMD > gpurun_out/plain_$c.log 2>&1 || { echo "plain $c failed"; continue; }

@@ -28,7 +28,7 @@ RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_sector_hit_rate.pct"]
 KERNEL_NAMES = {"rowwise": "rowwise_tma_dsmem", "flat_tma": "flat_tma", "hist": "hist256_lanepriv_tma",
-                "segmented": "segmented_csr", "generic": "generic"}
+                "segmented": "segmented_csr", "teams": "teams_threads", "stencil5": "stencil5_tma", "generic": "generic"}
 
 
 def unit_scale(unit: str) -> float:
