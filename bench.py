@@ -216,13 +216,14 @@ def run_hpar(args):
         alg_bytes = cnt * cols * 4 + cnt * 4
         host_in_bytes, host_out_bytes = cnt * cols * 4, cnt * 4
     elif kind in ("flat", "hist"):
+        nflags = H.HPAR_NEST_NODE_FUSED if (args.node == "fused" and comm is not None) else 0
         if kind == "flat":
             nest = H.Nest(nests.c5_nest(K), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
-                          clusters=args.clusters)
+                          clusters=args.clusters, flags=nflags)
         else:
             nest = H.Nest(nests.c4_nest(K, tile=int(os.environ.get("HPAR_C4_TILE", nests.TILE_U8))),
                           device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
-                          clusters=args.clusters)
+                          clusters=args.clusters, flags=nflags)
         b, cnt = nest.shard_range(spec["n0"], rank)
         if kind == "flat":
             x = torch.empty(cnt, dtype=torch.float32, device=dev)
@@ -240,7 +241,8 @@ def run_hpar(args):
         elems_rank = cnt
         host_out_bytes = out.numel() * out.element_size()
     elif kind == "c1":
-        nest = H.Nest(nests.c1_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W)
+        nest = H.Nest(nests.c1_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+                      flags=H.HPAR_NEST_NODE_FUSED if (args.node == "fused" and comm is not None) else 0)
         b, cnt = nest.shard_range(spec["n0"] * world, rank)
         x = torch.empty(cnt * 1024, dtype=torch.int32, device=dev)
         L.hpar_inputs_fill_i32(spec["seed"], b * 1024, cnt * 1024, x.data_ptr(), sptr)
@@ -364,7 +366,9 @@ def run_hpar(args):
         "config": {"workload": spec["workload"], "kernel": kernel, "n0_global": spec["n0"],
                    "elements_total": elems_total, "parallelism": f"gpu{world}",
                    "l2": "inputs > L2, no flush" if flush is None else "L2 flushed (256 MB write) before each step",
-                   "geometry": {"C": nest.info().C, "K": K, "W": W}},
+                   "geometry": {"C": nest.info().C, "K": K, "W": W},
+                   "node_level": ("in-kernel (NCCL LSA)" if args.node == "fused" else "ncclAllReduce")
+                   if world > 1 and kind in ("flat", "hist", "c1") else None},
         "hbm_gbs": achieved * (world if spec["scaling"] == "weak" else 1) if False else achieved,
         "pct_of_8tbs": achieved / NOMINAL_HBM_GBS,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -525,6 +529,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
     ap.add_argument("--impl", default="hpar", choices=["hpar", "reference"])
+    ap.add_argument("--node", default="nccl", choices=["nccl", "fused"],
+                    help="node level of total reductions at N>1: host ncclAllReduce, or in-kernel (NEXT f1)")
     ap.add_argument("--clusters", type=int, default=-1, help="C (0 = resident clusters, -1 = tuned default)")
     ap.add_argument("--warps", type=int, default=0, help="W warps per CTA (0 = tuned default)")
     ap.add_argument("--e2e-steps", type=int, default=10)

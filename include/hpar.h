@@ -176,11 +176,23 @@ typedef struct {
   int32_t rank, nranks;  /* used when nccl_comm == NULL (single GPU: 0 / 1)         */
   int32_t cluster_dim;   /* K CTAs per cluster; 0 = 2                               */
   int32_t warps_per_cta; /* W; 0 = 8                                                */
-  int32_t reserved;
+  int32_t flags;         /* HPAR_NEST_* options                                     */
   int64_t clusters;      /* C; 0 = derived (resident clusters)                      */
   void* nccl_comm;       /* borrowed ncclComm_t for the GPU level, or NULL          */
   const hpar_device_desc* desc; /* required when device == -1                       */
 } hpar_nest_config;
+
+/* flags: HPAR_NEST_NODE_FUSED — the node level runs inside
+ * the kernel instead of as a host-enqueued ncclAllReduce: the CTA that folds
+ * a GPU's total stores it into every rank's symmetric slot (NCCL LSA pointers
+ * over NVLink), all GPUs meet at one NCCL LSA barrier, and each folds the
+ * slots in rank order (so ordered ops stay ordered).  Needs nccl_comm; nest
+ * creation and destruction become COLLECTIVE over the communicator (NCCL
+ * window registration and device-communicator creation); all ranks must be
+ * in one NVLink domain (else HPAR_E_CAPABILITY); NCCL >= 2.28 (else
+ * HPAR_E_NCCL).  Applies to total-mode calls; keyed calls have no node
+ * level. */
+#define HPAR_NEST_NODE_FUSED 1
 
 typedef struct hpar_nest* hpar_nest_t;
 

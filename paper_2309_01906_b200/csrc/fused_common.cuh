@@ -2,6 +2,7 @@
 // kernels: level-structure matching and the end-of-kernel combine climb.
 #pragma once
 #include "level_primitives.cuh"
+#include "node_fused.cuh"
 #include "plan.h"
 
 namespace hpar {
@@ -84,9 +85,10 @@ __device__ void fused_total_climb(const NestArgs& a, Acc v, int W, ClimbSmem<Acc
     Acc* parts = (Acc*)a.cluster_partials;
     if (grid_arrive<Acc>(cluster_v, parts, a.grid_ticket, cl, a.C, &sh.flag)) {
       Acc tot = block_fold_ordered<OP, Acc>(parts, a.C, sh.warp);
+      if (threadIdx.x == 0) export_slot<Acc>(a, S_GPU, 0, tot);
+      if (a.node_dc) node_fold_scalar<OP, Acc>(a, tot);  // the node level in-kernel (f1)
       if (threadIdx.x == 0) {
         *(Acc*)a.out = tot;
-        export_slot<Acc>(a, S_GPU, 0, tot);
         *a.grid_ticket = 0u;
       }
     }

@@ -19,6 +19,7 @@
 #include <stdint.h>
 #include <type_traits>
 #include "level_primitives.cuh"
+#include "node_fused.cuh"
 #include "plan.h"
 
 namespace hpar {
@@ -319,14 +320,13 @@ struct Generic {
       Acc* parts = (Acc*)a.cluster_partials;
       if (grid_arrive<Acc>(acc, parts, a.grid_ticket, cl, a.C, &sh.flag)) {
         Acc tot = block_fold_ordered<OP, Acc>(parts, a.C, &sh.warp[0][0]);
+        if (threadIdx.x == 0 && !keyed && (a.verify & V_PARTIALS)) {
+          for (int l = 0; l < a.nlev; ++l)
+            if (a.lv[l].slast == S_GPU && a.partials[l]) ((Acc*)a.partials[l])[0] = tot;
+        }
+        if (!keyed && a.node_dc) node_fold_scalar<OP, Acc>(a, tot);  // the node level in-kernel (f1)
         if (threadIdx.x == 0) {
-          if (!keyed) {
-            *(Acc*)a.out = tot;
-            if ((a.verify & V_PARTIALS)) {
-              for (int l = 0; l < a.nlev; ++l)
-                if (a.lv[l].slast == S_GPU && a.partials[l]) ((Acc*)a.partials[l])[0] = tot;
-            }
-          }
+          if (!keyed) *(Acc*)a.out = tot;
           *a.grid_ticket = 0u;
         }
         for (int64_t s = threadIdx.x; s < a.dyn_slots; s += blockDim.x) a.dyn_tickets[s] = 0ull;

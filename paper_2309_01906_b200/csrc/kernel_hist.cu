@@ -225,14 +225,24 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
     }
     __syncthreads();
     if (s_flag) {
-      for (int bin = threadIdx.x; bin < 256; bin += blockDim.x) {
-        unsigned long long tot = 0;
-        for (int64_t c = 0; c < a.C; ++c) tot += ((volatile unsigned long long*)parts)[c * 256 + bin];
-        ((unsigned long long*)a.out)[bin] = tot;
+      constexpr int NB = 4;  // bins per thread (blockDim.x >= 64)
+      unsigned long long tot[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int bin = threadIdx.x + j * blockDim.x;
+        tot[j] = 0;
+        if (bin >= 256) continue;
+        for (int64_t c = 0; c < a.C; ++c) tot[j] += ((volatile unsigned long long*)parts)[c * 256 + bin];
         if (VERIFY && (a.verify & V_PARTIALS)) {
           for (int l = 0; l < a.nlev; ++l)
-            if (a.lv[l].slast == S_GPU && a.partials[l]) ((unsigned long long*)a.partials[l])[bin] = tot;
+            if (a.lv[l].slast == S_GPU && a.partials[l]) ((unsigned long long*)a.partials[l])[bin] = tot[j];
         }
+      }
+      if (a.node_dc) node_fold_bins<NB>(a, tot);  // the node level in-kernel (f1)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int bin = threadIdx.x + j * blockDim.x;
+        if (bin < 256) ((unsigned long long*)a.out)[bin] = tot[j];
       }
       if (threadIdx.x == 0) *a.grid_ticket = 0u;
     }

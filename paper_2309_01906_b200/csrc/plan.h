@@ -67,6 +67,15 @@ struct NestArgs {
   unsigned int* grid_ticket;
   void* cluster_partials;   // C accumulators (or C x 256 bins)
   int32_t* error_flag;
+
+  // fused node level (NEXT f1; node_fused.cuh): the CTA that produces this
+  // GPU's total stores it in every rank's symmetric slot [parity][rank],
+  // meets the other GPUs at an NCCL LSA barrier and folds the slots in rank
+  // order.  node_dc == NULL: the host enqueues NCCL instead.
+  const void* node_dc;    // ncclDevComm (device copy)
+  void* node_win;         // ncclWindow_t of the slot buffer
+  int32_t node_parity;    // which half of the slot buffer this call uses
+  int32_t node_slot;      // bytes per rank slot
 };
 
 }  // namespace hpar

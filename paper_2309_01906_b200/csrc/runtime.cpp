@@ -19,7 +19,8 @@
 #include <vector>
 
 #include "hpar.h"
-#include "nccl.h"  // types only; functions are resolved with dlsym
+#include "nccl.h"         // types only; functions are resolved with dlsym
+#include "nccl_device.h"  // ncclDevComm (fused node level, NEXT f1)
 #include "plan.h"
 
 namespace hpar {
@@ -88,6 +89,13 @@ struct NcclApi {
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
+  // symmetric memory + device communicator (NCCL >= 2.28): fused node level
+  ncclResult_t (*memAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*memFree)(void*) = nullptr;
+  ncclResult_t (*winRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+  ncclResult_t (*winDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
+  ncclResult_t (*devCommCreate)(ncclComm_t, const ncclDevCommRequirements_t*, ncclDevComm_t*) = nullptr;
+  ncclResult_t (*devCommDestroy)(ncclComm_t, const ncclDevComm_t*) = nullptr;
 };
 NcclApi g_nccl;
 std::once_flag g_nccl_once;
@@ -111,6 +119,12 @@ void load_nccl() {
   g_nccl.recv = (decltype(g_nccl.recv))dlsym(h, "ncclRecv");
   g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
   g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
+  g_nccl.memAlloc = (decltype(g_nccl.memAlloc))dlsym(h, "ncclMemAlloc");
+  g_nccl.memFree = (decltype(g_nccl.memFree))dlsym(h, "ncclMemFree");
+  g_nccl.winRegister = (decltype(g_nccl.winRegister))dlsym(h, "ncclCommWindowRegister");
+  g_nccl.winDeregister = (decltype(g_nccl.winDeregister))dlsym(h, "ncclCommWindowDeregister");
+  g_nccl.devCommCreate = (decltype(g_nccl.devCommCreate))dlsym(h, "ncclDevCommCreate");
+  g_nccl.devCommDestroy = (decltype(g_nccl.devCommDestroy))dlsym(h, "ncclDevCommDestroy");
   g_nccl.loaded = g_nccl.allReduce && g_nccl.commCount && g_nccl.commUserRank && g_nccl.getErrorString;
   if (!g_nccl.loaded) g_nccl.why = "libnccl.so.2 lacks required symbols";
 }
@@ -272,6 +286,14 @@ struct hpar_nest {
   size_t seg_ws_bytes = 0;
   float* halo_buf = nullptr;  // ghost exchange staging (grown on demand)
   size_t halo_bytes = 0;
+  // fused node level (HPAR_NEST_NODE_FUSED; node_fused.cuh)
+  bool node_fused = false;
+  void* node_sym = nullptr;         // symmetric slot buffer (ncclMemAlloc)
+  ncclWindow_t node_win = nullptr;  // its NCCL window
+  ncclDevComm node_dc;              // device communicator (host copy)
+  bool node_dc_made = false;
+  void* node_dc_dev = nullptr;      // device copy of node_dc
+  uint64_t node_calls = 0;
 };
 
 namespace {
@@ -289,6 +311,41 @@ int slot_last(int hw, bool partitioned) {
 const char* sched_name(int s) {
   static const char* n[] = {"static", "static(c)", "dynamic(c)", "none"};
   return (s >= 0 && s < 4) ? n[s] : "?";
+}
+}  // namespace
+
+namespace {
+// Fused node level (NEXT f1): one symmetric slot buffer per rank ([2 halves]
+// x [G ranks] x 2 KB, enough for 256 u64 bins), registered as an NCCL window,
+// and a device communicator with one LSA barrier.  Collective over the
+// communicator; every rank must sit in one NVLink (LSA) domain.
+constexpr size_t kNodeSlot = 2048;
+hpar_status node_fused_setup(hpar_nest* n) {
+  if (!n->comm) return fail(HPAR_E_INVALID, "HPAR_NEST_NODE_FUSED needs an NCCL communicator");
+  if (n->device < 0) return fail(HPAR_E_INVALID, "HPAR_NEST_NODE_FUSED needs a device");
+  if (hpar_status s = need_nccl()) return s;
+  if (!g_nccl.memAlloc || !g_nccl.winRegister || !g_nccl.devCommCreate || !g_nccl.devCommDestroy)
+    return fail(HPAR_E_NCCL, "NCCL lacks the device API (ncclDevCommCreate / windows: NCCL >= 2.28)");
+  ncclComm_t comm = (ncclComm_t)n->comm;
+  const size_t bytes = ((2 * (size_t)n->nranks * kNodeSlot + 4095) / 4096) * 4096;
+  ncclResult_t r = g_nccl.memAlloc(&n->node_sym, bytes);
+  if (r != ncclSuccess) return nccl_fail(r, comm, "ncclMemAlloc");
+  CUDA_TRY(cudaMemset(n->node_sym, 0, bytes));
+  r = g_nccl.winRegister(comm, n->node_sym, bytes, &n->node_win, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) return nccl_fail(r, comm, "ncclCommWindowRegister");
+  ncclDevCommRequirements req;
+  memset(&req, 0, sizeof(req));
+  req.lsaBarrierCount = 1;
+  r = g_nccl.devCommCreate(comm, &req, &n->node_dc);
+  if (r != ncclSuccess) return nccl_fail(r, comm, "ncclDevCommCreate");
+  n->node_dc_made = true;
+  if (n->node_dc.lsaSize != n->node_dc.nRanks)
+    return fail(HPAR_E_CAPABILITY, "fused node level: the %d ranks span more than one NVLink domain (LSA team of %d)",
+                n->node_dc.nRanks, n->node_dc.lsaSize);
+  CUDA_TRY(cudaMalloc(&n->node_dc_dev, sizeof(ncclDevComm)));
+  CUDA_TRY(cudaMemcpy(n->node_dc_dev, &n->node_dc, sizeof(ncclDevComm), cudaMemcpyHostToDevice));
+  n->node_fused = true;
+  return HPAR_OK;
 }
 }  // namespace
 
@@ -489,12 +546,29 @@ extern "C" hpar_status hpar_nest_create(const hpar_nest_level* lv, int32_t nleve
                   cudaGetErrorString(e));
     }
   }
+  // ---- fused node level (NEXT f1): collective over the communicator ----
+  if (cfg->flags & HPAR_NEST_NODE_FUSED) {
+    hpar_status s = node_fused_setup(n);
+    if (s) {
+      hpar_nest_destroy(n);
+      return s;
+    }
+  }
   *out = n;
   return ok();
 }
 
 extern "C" hpar_status hpar_nest_destroy(hpar_nest_t n) {
   if (!n) return ok();
+  if (n->device >= 0 && n->comm) {  // fused node level: collective teardown
+    cudaSetDevice(n->device);
+    cudaDeviceSynchronize();
+    ncclComm_t comm = (ncclComm_t)n->comm;
+    if (n->node_dc_made && g_nccl.devCommDestroy) g_nccl.devCommDestroy(comm, &n->node_dc);
+    if (n->node_win && g_nccl.winDeregister) g_nccl.winDeregister(comm, n->node_win);
+    if (n->node_sym && g_nccl.memFree) g_nccl.memFree(n->node_sym);
+    cudaFree(n->node_dc_dev);
+  }
   if (n->device >= 0) {
     cudaSetDevice(n->device);
     cudaFree(n->grid_ticket);
@@ -675,6 +749,13 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   A.dyn_tickets = n->dyn_tickets;
   A.dyn_slots = n->dyn_slots;
   A.dyn_level = -1;
+  const bool node_in_kernel = n->node_fused && !d->keyed;
+  if (node_in_kernel) {
+    A.node_dc = n->node_dc_dev;
+    A.node_win = n->node_win;
+    A.node_parity = (int32_t)(n->node_calls++ & 1);
+    A.node_slot = (int32_t)kNodeSlot;
+  }
 
   if ((d->verify & HPAR_VERIFY_COVERAGE) && (!d->coverage_owner || !d->coverage_count))
     return fail(HPAR_E_INVALID, "verify coverage needs coverage_owner and coverage_count");
@@ -784,7 +865,9 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   n->last_kernel = name;
 
   // ---- node level: one allreduce over NVLink (§8(a) A9) ----
-  if (!d->keyed && n->nranks > 1 && affine) {
+  if (node_in_kernel) {
+    // done inside the kernel (f1)
+  } else if (!d->keyed && n->nranks > 1 && affine) {
     // an ordered op cannot be an NCCL reduction: gather the per-rank results
     // in rank order (= the GPU level's static-block order) and fold them
     hpar_status s = need_nccl();

@@ -76,7 +76,7 @@ class NestLevel(ctypes.Structure):
 
 class NestConfig(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("cluster_dim", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("cluster_dim", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("clusters", ctypes.c_int64), ("nccl_comm", ctypes.c_void_p), ("desc", ctypes.POINTER(DeviceDesc))]
 
 
@@ -262,11 +262,11 @@ class Nest:
 
     def __init__(self, levels: list[Level], device: int = 0, nccl_comm: int | None = None, cluster_dim: int = 0,
                  warps_per_cta: int = 0, clusters: int = 0, rank: int = 0, nranks: int = 1,
-                 desc: DeviceDesc | None = None):
+                 desc: DeviceDesc | None = None, flags: int = 0):
         self.levels = list(levels)
         arr = (NestLevel * len(levels))(*[l.c() for l in levels])
         self._desc = desc
-        cfg = NestConfig(device, rank, nranks, cluster_dim, warps_per_cta, 0, clusters, nccl_comm,
+        cfg = NestConfig(device, rank, nranks, cluster_dim, warps_per_cta, flags, clusters, nccl_comm,
                          ctypes.pointer(desc) if desc is not None else None)
         h = ctypes.c_void_p()
         _check(lib().hpar_nest_create(arr, len(levels), ctypes.byref(cfg), ctypes.byref(h)))
@@ -407,3 +407,5 @@ def hpar_map_exchange(nest: "Nest", m: MapSpec, buf, ld: int, stream: int = 0) -
 def hpar_map_exchange_local(m: MapSpec, bufs: list, ld: int, stream: int = 0) -> None:
     arr = (ctypes.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs])
     _check(lib().hpar_map_exchange_local(ctypes.byref(m), arr, ld, ctypes.c_void_p(stream)))
+
+HPAR_NEST_NODE_FUSED = 1  # hpar_nest_config.flags: the node level inside the kernel (NEXT f1)
