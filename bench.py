@@ -116,11 +116,9 @@ def config_spec(name: str, nranks: int):
     if name == "c1":
         return dict(workload="c1_2level_1024x1024_i32", kind="c1", n0=1024, cols=1024, scaling="weak",
                     seed=gen.SEED_C1, dtype="i32", elems_per_rank=1 << 20, bytes_per_rank=(1 << 22) + 8)
-    if name == "c3":
+    if name == "c3":  # one 2^24-row matrix; rows sharded at nnz-balanced boundaries (§8(e))
         return dict(workload="c3_csr_segmented_2^24rows_2^28nnz_f32", kind="csr", rows=1 << 24, nnz=1 << 28,
-                    n0=(1 << 24) * nranks,
-                    scaling="weak", seed=gen.SEED_C3, dtype="f32", elems_per_rank=1 << 28,
-                    bytes_per_rank=(1 << 30) + ((1 << 24) + 1) * 8 + (1 << 24) * 4)
+                    n0=1 << 24, scaling="strong", seed=gen.SEED_C3, dtype="f32", elems_total=1 << 28)
     if name == "c6":  # NEXT f3: §4 ghost maps + 5-point stencil, one Jacobi sweep per step
         tile = 16384
         return dict(workload="c6_stencil5_16384x16384_per_gpu_f32", kind="stencil", tile=tile, n0=tile * tile,
@@ -257,16 +255,18 @@ def run_hpar(args):
         off_host = gen.csr_offsets(rows, nnz)
         nest = H.Nest(nests.c3_fast_nest(lane_chunk=int(os.environ.get("HPAR_C3_LPL", "16"))), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
                       clusters=args.clusters)
-        b, cnt = nest.shard_range(rows * world, rank)  # each rank: its own copy of the matrix (weak)
-        off = torch.from_numpy(off_host).to(dev)
-        x = torch.empty(nnz, dtype=torch.float32, device=dev)
-        L.hpar_inputs_fill_f32(spec["seed"], rank * nnz, nnz, x.data_ptr(), sptr)
-        out = torch.empty(rows, dtype=torch.float32, device=dev)
-        desc = H.make_desc(x, out, n0=rows * world, n1=nnz, nloops=2, keyed=True, offsets=off,
-                           max_inner=int((off_host[1:] - off_host[:-1]).max()))
-        elems_rank = nnz
-        alg_bytes = nnz * 4 + (rows + 1) * 8 + rows * 4
-        host_in_bytes, host_out_bytes = nnz * 4 + (rows + 1) * 8, rows * 4
+        b, cnt = H.hpar_shard_range_csr(off_host, world, rank)  # nnz-balanced row shard
+        lo = off_host[b:b + cnt + 1] - off_host[b]
+        nnz_l = int(lo[-1])
+        off = torch.from_numpy(lo).to(dev)
+        x = torch.empty(max(nnz_l, 4), dtype=torch.float32, device=dev)
+        L.hpar_inputs_fill_f32(spec["seed"], int(off_host[b]), nnz_l, x.data_ptr(), sptr)  # global indices
+        out = torch.empty(max(cnt, 1), dtype=torch.float32, device=dev)
+        desc = H.make_desc(x, out, n0=rows, n1=nnz_l, nloops=2, keyed=True, offsets=off, local_n0=cnt,
+                           max_inner=int((lo[1:] - lo[:-1]).max()) if cnt else 0)
+        elems_rank = nnz_l
+        alg_bytes = nnz_l * 4 + (cnt + 1) * 8 + cnt * 4
+        host_in_bytes, host_out_bytes = nnz_l * 4 + (cnt + 1) * 8, cnt * 4
         extra_inputs = [off]
     torch.cuda.synchronize()
 
@@ -316,7 +316,7 @@ def run_hpar(args):
     step_ms = float(t.item())
     elems_total = elems_rank * world if spec["scaling"] == "weak" else spec["n0"] * (1024 if kind == "c1" else 1)
     if spec["scaling"] == "strong":
-        elems_total = spec["n0"]
+        elems_total = spec.get("elems_total", spec["n0"])
     value = elems_total / (step_ms * 1e-3)
     peak, peak_src = measured_peak()
     achieved = alg_bytes / (step_ms_local * 1e-3) / 1e9
@@ -514,7 +514,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": spec["scaling"], "vs_baseline": None, "dtype": spec["dtype"],
         "data": "synthetic (seeded splitmix64, inputs/gen.py recipe)",
-        "config": {"workload": spec["workload"], "kernel": "oracle (CPU, sequential C)"},
+        "config": {"workload": spec["workload"],
+                   "kernel": "oracle (CPU, numpy fp32)" if args.config == "c6" else "oracle (CPU, sequential C)"},
         "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle",
                          "sample": f"{what} per step, {args.steps} timed steps, {dt:.1f} s"},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

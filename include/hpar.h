@@ -267,7 +267,20 @@ typedef struct {
   uint32_t* coverage_count; /* verify: per local iteration, visit count (caller zeroes)    */
   uint64_t* fingerprint;    /* verify: uint64[3] += {F_once, F_owner, iterations}         */
   uint64_t global_begin;    /* global index of this rank's first iteration (fingerprints) */
+  int64_t local_n0;         /* CSR only: this rank's row count when the caller shards rows
+                               by nonzeros (hpar_shard_range_csr); 0 = the GPU level's
+                               static block of n0.  A rank whose shard is empty skips the
+                               call (keyed results have no node-level collective)         */
 } hpar_reduce_desc;
+
+/* §8(e) C3: nnz-balanced contiguous row shards of a CSR matrix over
+ * `nranks` GPUs — the GPU level's static block weighted by nonzeros.  Rank g
+ * gets rows [b_g, b_{g+1}) with b_g = the first row whose start offset is
+ * >= ceil(g * nnz / nranks) (b_0 = 0, b_nranks = rows), so every shard holds
+ * nnz / nranks nonzeros up to one row.  `offsets`: HOST int64 [rows + 1],
+ * nondecreasing from 0.  Pure host. */
+hpar_status hpar_shard_range_csr(const int64_t* offsets, int64_t rows, int32_t nranks, int32_t rank,
+                                 int64_t* begin, int64_t* count);
 
 /* §8(a) A2-A9: execute the nest over the loop(s) in `desc` and reduce.
  * One launch of a kernel specialisation picked by the planner (the generic

@@ -493,8 +493,11 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
           const int sc = min(max(s_ - wr, 0), WIN);
           const int ec = min(max(e_ - wr, sc), WIN);
           if (exact) {
+            // an odd end / start adds the one value before it (the array's
+            // unaligned tail is not in the ring: read it directly)
+            auto at = [&](int q) -> float { return (wr + q >= lim4) ? x[base + wr + q] : sm.ring[s][q]; };
             val = (e_even<LPL>(sm, ec & ~1) - e_even<LPL>(sm, sc & ~1)) +
-                  ((double)((ec & 1) ? sm.ring[s][ec - 1] : 0.f) - (double)((sc & 1) ? sm.ring[s][sc - 1] : 0.f));
+                  ((double)((ec & 1) ? at(ec - 1) : 0.f) - (double)((sc & 1) ? at(sc - 1) : 0.f));
           } else {
             for (int q = sc; q < ec; ++q) val += (double)((wr + q >= lim4) ? x[base + wr + q] : sm.ring[s][q]);
           }
@@ -572,6 +575,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
   // the race waits for its entry.  Leave once every block is done (no entry
   // can appear any more) and the queue is drained.  Idle polling backs off.
   unsigned nap = 32;
+  const unsigned nap_max = (dbg >> 8) ? (unsigned)(dbg >> 8) : 2048u;  // (knob: HPAR_SEG_DEBUG bits 8+)
   unsigned long long dbg_nseg = 0, dbg_tseg = 0, dbg_tdone = 0;
   for (;;) {
     unsigned long long head = 0, tail = 0, done = 0;
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       break;
     }
     __nanosleep(nap);
-    nap = nap < 2048 ? 2 * nap : 2048;
+    nap = nap < nap_max ? 2 * nap : nap_max;
   }
 
   if (ws.dbg_t && lane == 0) ws.dbg_t[6 * gwarp + 2] = gtimer();

@@ -625,6 +625,23 @@ void shard_of(const hpar_nest* n, int64_t n0, int32_t rank, int64_t* begin, int6
 }
 }  // namespace
 
+extern "C" hpar_status hpar_shard_range_csr(const int64_t* off, int64_t rows, int32_t nranks, int32_t rank,
+                                            int64_t* begin, int64_t* count) {
+  if (!off || rows < 0 || nranks < 1 || rank < 0 || rank >= nranks || !begin || !count)
+    return fail(HPAR_E_INVALID, "hpar_shard_range_csr: bad arguments");
+  const int64_t nnz = off[rows];
+  auto bound = [&](int32_t g) -> int64_t {  // first row whose start >= ceil(g * nnz / nranks)
+    if (g <= 0) return 0;
+    if (g >= nranks) return rows;
+    const int64_t target = (int64_t)(((__int128)g * nnz + nranks - 1) / nranks);
+    return (int64_t)(std::lower_bound(off, off + rows, target) - off);
+  };
+  const int64_t b = bound(rank), e = bound(rank + 1);
+  *begin = b;
+  *count = e > b ? e - b : 0;
+  return ok();
+}
+
 extern "C" hpar_status hpar_shard_range(hpar_nest_t n, int64_t n0, int32_t rank, int64_t* begin, int64_t* count) {
   if (!n || !begin || !count) return fail(HPAR_E_INVALID, "hpar_shard_range: NULL argument");
   if (rank < 0 || rank >= n->nranks) return fail(HPAR_E_INVALID, "rank %d out of range", rank);
@@ -696,6 +713,11 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
 
   int64_t begin = 0, local = 0;
   shard_of(n, d->n0, n->rank, &begin, &local);
+  if (d->local_n0 > 0) {  // caller-sharded CSR rows (hpar_shard_range_csr, §8(e) C3)
+    if (!d->offsets || !d->keyed || d->local_n0 > d->n0)
+      return fail(HPAR_E_INVALID, "local_n0 is for keyed CSR calls (and <= n0)");
+    local = d->local_n0;
+  }
   if (local > 0 && !d->in) return fail(HPAR_E_INVALID, "in is NULL");
 
   // ---- schedule(none) overflow (diagnose, never UB) ----

@@ -100,7 +100,7 @@ class ReduceDesc(ctypes.Structure):
                 ("max_inner", ctypes.c_int64), ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
                 ("verify", ctypes.c_int32), ("level_partials", ctypes.c_void_p * MAX_NEST),
                 ("coverage_owner", ctypes.c_void_p), ("coverage_count", ctypes.c_void_p),
-                ("fingerprint", ctypes.c_void_p), ("global_begin", ctypes.c_uint64)]
+                ("fingerprint", ctypes.c_void_p), ("global_begin", ctypes.c_uint64), ("local_n0", ctypes.c_int64)]
 
 
 class MapDim(ctypes.Structure):
@@ -155,6 +155,8 @@ def lib() -> ctypes.CDLL:
             "hpar_nest_resolve": [ctypes.POINTER(SyncConstruct), ctypes.c_int32, ctypes.POINTER(LevelInfo),
                                   ctypes.POINTER(NestLevel)],
             "hpar_level_alias": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
+            "hpar_shard_range_csr": [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)],
             "hpar_map_sections": [ctypes.POINTER(MapSpec), ctypes.c_int32, ctypes.POINTER(Rect), ctypes.POINTER(Rect)],
             "hpar_map_validate": [ctypes.POINTER(MapSpec), ctypes.POINTER(ctypes.c_int64)],
             "hpar_map_exchange_plan": [ctypes.POINTER(MapSpec), ctypes.c_int32, ctypes.POINTER(Halo), ctypes.c_int32,
@@ -327,7 +329,8 @@ def dtype_code(t) -> int:
 
 def make_desc(x, out, *, op: int = OP_SUM, n0: int, n1: int = 0, ld: int = 0, nloops: int = 1,
               keyed: bool = False, offsets=None, max_inner: int = 0, out_dtype: int = -1, verify: int = 0,
-              partials=None, owner=None, count=None, fingerprint=None, global_begin: int = 0) -> ReduceDesc:
+              partials=None, owner=None, count=None, fingerprint=None, global_begin: int = 0,
+              local_n0: int = 0) -> ReduceDesc:
     """Build an hpar_reduce_desc from torch tensors (device pointers only)."""
     d = ReduceDesc()
     d.op = op
@@ -347,6 +350,7 @@ def make_desc(x, out, *, op: int = OP_SUM, n0: int, n1: int = 0, ld: int = 0, nl
     d.coverage_count = count.data_ptr() if count is not None else None
     d.fingerprint = fingerprint.data_ptr() if fingerprint is not None else None
     d.global_begin = global_begin
+    d.local_n0 = local_n0
     return d
 
 
@@ -409,3 +413,12 @@ def hpar_map_exchange_local(m: MapSpec, bufs: list, ld: int, stream: int = 0) ->
     _check(lib().hpar_map_exchange_local(ctypes.byref(m), arr, ld, ctypes.c_void_p(stream)))
 
 HPAR_NEST_NODE_FUSED = 1  # hpar_nest_config.flags: the node level inside the kernel (NEXT f1)
+
+
+def hpar_shard_range_csr(offsets, nranks: int, rank: int) -> tuple[int, int]:
+    """nnz-balanced row shard (§8(e) C3); offsets: host int64 numpy [rows + 1]."""
+    import numpy as np
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    b, c = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().hpar_shard_range_csr(off.ctypes.data, off.size - 1, nranks, rank, ctypes.byref(b), ctypes.byref(c)))
+    return b.value, c.value

@@ -337,9 +337,13 @@ def _csr_cases():
     off[1:] = np.cumsum(lens)
     yield "edges", off
     yield "short_only", np.arange(0, 2 * 70001, 2, dtype=np.int64)
+    # nnz % 4 != 0 with short rows at the very end: the unaligned array tail
+    # (< 4 values past the last whole 16 bytes) at odd and even row ends
+    tail = np.concatenate([[0], np.cumsum(np.tile([3, 1, 16, 2, 5, 1, 1], 1001))]).astype(np.int64)
+    yield "unaligned_tail", tail
 
 
-@pytest.mark.parametrize("case", ["zipf", "all_empty", "one_huge_row", "edges", "short_only"])
+@pytest.mark.parametrize("case", ["zipf", "all_empty", "one_huge_row", "edges", "short_only", "unaligned_tail"])
 def test_segmented_csr_kernel(H, torch_mod, oracle, case):
     """Config-3 fused kernel: every row sum within 1e-5 of the oracle's fp64
     segment sums (0 exactly for empty rows), every nonzero visited once, each
@@ -462,3 +466,30 @@ def test_generic_keyed_dynamic_repeated_calls(H, torch_mod, oracle):
             torch.cuda.synchronize()
             assert (count.cpu().numpy() == 1).all()
             assert_rel(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_segmented_nnz_balanced_ranks(H, torch_mod, oracle, G):
+    """§8(e) C3: the GPU level shards rows at nnz-balanced boundaries
+    (hpar_shard_range_csr); each rank's call sees only its rows (local_n0)
+    and values; the concatenated keyed results equal the oracle.  The ranks
+    run one after another on this GPU (keyed results: no node collective)."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    off = gen.csr_offsets(20000, 300000)
+    v = gen.gen_f32(gen.SEED_C3, 0, int(off[-1]))
+    got = np.full(20000, np.nan)
+    for g in range(G):
+        b, c = H.hpar_shard_range_csr(off, G, g)
+        nest = H.Nest(nests.c3_fast_nest(), device=0, rank=g, nranks=G, cluster_dim=2, warps_per_cta=8, clusters=5)
+        lo = (off[b:b + c + 1] - off[b]).astype(np.int64)
+        vals = v[off[b]:off[b + c]]
+        xd = torch.from_numpy(vals).cuda() if vals.size else torch.zeros(4, dtype=torch.float32, device="cuda")
+        out = torch.full((max(c, 1),), -1.0, dtype=torch.float64, device="cuda")
+        d = H.make_desc(xd, out, n0=20000, n1=int(vals.size), nloops=2, keyed=True,
+                        offsets=torch.from_numpy(lo).cuda(), out_dtype=H.F64, local_n0=c)
+        nest.parallel_for_reduce(d)
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "segmented_csr"
+        got[b:b + c] = out.cpu().numpy()[:c]
+    assert_rel(got, oracle.segsum_f32(v, off))

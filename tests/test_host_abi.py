@@ -158,3 +158,30 @@ def test_shard_ranges(H):
                     assert b == prev and c >= 0
                     prev = b + c
                 assert prev == n0
+
+
+def test_shard_range_csr_is_nnz_balanced(H):
+    """§8(e) C3: contiguous, covering row shards whose nonzero counts differ
+    from nnz/G by less than one row (brute force over the definition)."""
+    import numpy as np
+    from inputs import gen
+    rng = np.random.default_rng(3)
+    cases = [gen.csr_offsets(5000, 70000), np.zeros(11, np.int64), np.array([0, 10**6], np.int64)]
+    lens = rng.integers(0, 50, 777)
+    cases.append(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64))
+    for off in cases:
+        rows, nnz = off.size - 1, int(off[-1])
+        for G in (1, 2, 3, 4, 8):
+            shards = [H.hpar_shard_range_csr(off, G, g) for g in range(G)]
+            assert shards[0][0] == 0 and sum(c for _, c in shards) == rows
+            for (b0, c0), (b1, _) in zip(shards, shards[1:]):
+                assert b0 + c0 == b1
+            for g, (b, c) in enumerate(shards):
+                # the definition: b_g = first row whose start offset >= ceil(g nnz / G)
+                target = -(-g * nnz // G)
+                hit = np.nonzero(off[:rows] >= target)[0]
+                want = 0 if g == 0 else (int(hit[0]) if hit.size else rows)
+                assert b == want
+                if rows and nnz:
+                    maxlen = int(np.diff(off).max())
+                    assert abs(int(off[b + c] - off[b]) - nnz / G) <= maxlen + 1
