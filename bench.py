@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "elements/s and HBM GB/s (% of peak) for nested reductions at 1/2/4/8 B200"
 NOMINAL_HBM_GBS = 8000.0
+RED_SHARED_PEAK_UPS = 5.764e12  # red.shared.add.u32, lane-private (profiles/r01_red_shared_peak.txt)
 L2_BYTES = 126 * 2 ** 20
 
 
@@ -376,6 +377,11 @@ def run_hpar(args):
                      "algorithmic_bytes_per_launch": int(alg_bytes)},
         "clocks": clk, "e2e": e2e, "gpu_launches": args.steps,
     }
+    if kind == "hist":  # the second ceiling: shared-memory RED throughput (profiles/r01_red_shared_peak.txt)
+        ups = elems_rank / (step_ms_local * 1e-3)
+        line["roofline_smem_red"] = {"bound": "smem_red", "achieved": ups, "peak": RED_SHARED_PEAK_UPS,
+                                     "unit": "updates/s", "frac": ups / RED_SHARED_PEAK_UPS,
+                                     "peak_source": "measured, scripts/red_shared_peak.cu"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
     if rank == 0:
