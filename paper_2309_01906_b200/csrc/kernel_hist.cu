@@ -7,12 +7,15 @@
 //     warp     static(512)       (32 lanes x 16 B)
 //     lane     static(16)
 // Privatisation per level:
-//     lane    : its own 256 u32 counters, laid out counts[bin][lane] in the
-//               warp's shared-memory table, so lane l always hits bank l: no
-//               bank conflicts and no two lanes on one address, whatever the
-//               data (skewed or all-zero inputs cost the same).  Increments
-//               are fire-and-forget shared atomics (red.shared, no return
-//               value), so consecutive bytes of a lane never wait on each other.
+//     lane    : its own 256 u32 counters.  Warps 2p and 2p+1 share a 64 KiB
+//               region laid out [bin][warp & 1][lane] (256-byte bin rows), so
+//               lane l always hits bank l: no bank conflicts and no two lanes
+//               on one address, whatever the data (skewed or all-zero inputs
+//               cost the same).  A counter's offset in the region is
+//               bin << 8 | (warp & 1) << 7 | lane << 2: ONE byte permute
+//               (PRMT) of the data word with the lane's column gives it, so an
+//               increment is PRMT + one fire-and-forget shared atomic
+//               (red.shared, no return value).
 //     warp    : sum of its 32 lanes' counters (rotated reads, conflict-free)
 //     CTA     : sum of its warps' bins (ascending warp), bar.sync
 //     cluster : reduce-scatter over DSMEM — CTA k owns bins [256k/K, 256(k+1)/K)
@@ -23,13 +26,19 @@
 // Input stream: producer warp + 1-D TMA bulk ring as in kernel_flat.cu.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 #include "fused_common.cuh"
 
 namespace hpar {
 namespace {
 
 constexpr int kStages = 5;  // 5 x 16 KiB in flight per CTA next to 4 x 32 KiB lane tables
-constexpr int kMaxW = 6;  // 6 x 32 KiB lane tables + the ring fit in 227 KiB
+constexpr int kMaxW = 6;  // 3 x 64 KiB lane-table regions + the ring fit in 227 KiB
+constexpr int kRegion = 65536;  // lane tables of a warp pair
+
+__device__ __forceinline__ size_t table_bytes(int W) { return (size_t)((W + 1) / 2) * kRegion; }
+// offset of counter (bin, lane) of `warp` inside its pair's region, in words
+__device__ __forceinline__ int tab_word(int bin, int warp, int lane) { return bin * 64 + (warp & 1) * 32 + lane; }
 
 __device__ __forceinline__ void inc_shared(uint32_t addr) {
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
@@ -54,9 +63,13 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
   const int K = a.K;
   const uint32_t crank = cluster_ctarank();
   const int64_t cl = blockIdx.x / K;
-  uint32_t* counts = (uint32_t*)(dsm + (size_t)kStages * tile);  // [W][256][32]
+  // dynamic smem: the lane-table regions first (their shared addresses are
+  // link-time constants, so a region base folds into the atomic's immediate
+  // offset), then the TMA ring
+  uint32_t* counts = (uint32_t*)dsm;  // [W/2][256][2][32]
+  unsigned char* ring = dsm + table_bytes(W);
 
-  for (int i = threadIdx.x; i < W * 256 * 32; i += blockDim.x) counts[i] = 0;
+  for (int i = threadIdx.x; i < (int)(table_bytes(W) / 4); i += blockDim.x) counts[i] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -77,13 +90,19 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
         const int64_t len = (n - base < tile) ? (n - base) : tile;
         const uint32_t bytes = (uint32_t)(len & ~(int64_t)15);
         mbar_arrive_expect_tx(&full[s], bytes);
-        if (bytes) bulk_g2s(dsm + (size_t)s * tile, x + base, bytes, &full[s], pol);
+        if (bytes) bulk_g2s(ring + (size_t)s * tile, x + base, bytes, &full[s], pol);
         if (++s == kStages) { s = 0; ph ^= 1; }
       }
     }
   } else {
-    // this lane's column of the warp's table: word (bin*32 + lane)
-    const uint32_t col = smem_addr(counts + (size_t)warp * 256 * 32 + lane);
+   // the pair's region (a compile-time constant per PAIR instance) and this
+   // lane's column (byte 0 of every counter offset; PRMT puts the data byte
+   // in byte 1): an increment is PRMT + RED [reg + imm]
+   auto consume = [&](auto pair_c) {
+    constexpr int PAIR = decltype(pair_c)::value;
+    const uint32_t region = smem_addr(dsm) + (uint32_t)PAIR * kRegion;
+    const uint32_t col = (uint32_t)((warp & 1) * 128 + lane * 4);
+#define HPAR_INC(w, k) inc_shared(region + __byte_perm((w), col, 0x5504u | ((k) << 4)))
     const int nvec = tile / 16;
     const int64_t leaf = (int64_t)a.rank * a.threads_per_gpu + b * W * 32 + threadIdx.x;
     int s = 0;
@@ -92,7 +111,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
       const int64_t base = (j * nblocks + b) * tile;
       const int64_t len = (n - base < tile) ? (n - base) : tile;
       mbar_wait(&full[s], ph);
-      const unsigned char* st = dsm + (size_t)s * tile;
+      const unsigned char* st = ring + (size_t)s * tile;
       if (len == tile && VPL > 0) {
         // all of this lane's vectors of the tile first (ILP over the smem
         // latency), then the increments
@@ -105,10 +124,10 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t w = w4[k];
-            inc_shared(col + ((w << 7) & 0x7F80u));   // byte 0 -> bin*128
-            inc_shared(col + ((w >> 1) & 0x7F80u));   // byte 1
-            inc_shared(col + ((w >> 9) & 0x7F80u));   // byte 2
-            inc_shared(col + ((w >> 17) & 0x7F80u));  // byte 3
+            HPAR_INC(w, 0);
+            HPAR_INC(w, 1);
+            HPAR_INC(w, 2);
+            HPAR_INC(w, 3);
           }
         }
         if constexpr (VERIFY) {
@@ -126,10 +145,10 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t w = w4[k];
-            inc_shared(col + ((w << 7) & 0x7F80u));   // byte 0 -> bin*128
-            inc_shared(col + ((w >> 1) & 0x7F80u));   // byte 1
-            inc_shared(col + ((w >> 9) & 0x7F80u));   // byte 2
-            inc_shared(col + ((w >> 17) & 0x7F80u));  // byte 3
+            HPAR_INC(w, 0);
+            HPAR_INC(w, 1);
+            HPAR_INC(w, 2);
+            HPAR_INC(w, 3);
           }
           if constexpr (VERIFY) {
             for (int e = 0; e < 16; ++e) {
@@ -145,7 +164,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
             const int64_t off = 16 * (int64_t)f + e;
             if (off >= len) break;
             const uint32_t byte = off < in_smem ? st[off] : x[base + off];
-            inc_shared(col + (byte << 7));
+            inc_shared(region + col + (byte << 8));
             if constexpr (VERIFY) {
               if (a.verify & V_COVERAGE) { a.owner[base + off] = leaf; atomicAdd(&a.count[base + off], 1u); }
             }
@@ -156,18 +175,25 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == kStages) { s = 0; ph ^= 1; }
     }
+   };
+    switch (warp >> 1) {
+      case 0: consume(std::integral_constant<int, 0>()); break;
+      case 1: consume(std::integral_constant<int, 1>()); break;
+      default: consume(std::integral_constant<int, 2>()); break;
+    }
   }
   __syncwarp();
   __syncthreads();
+#undef HPAR_INC
   // lane -> warp: warp w sums the 32 lane columns of its table; lane l owns
   // bins l, l+32, ...; rotated column order keeps the reads conflict-free
   if (warp < W) {
-    const uint32_t* tab = counts + (size_t)warp * 256 * 32;
+    const uint32_t* tab = counts + (size_t)(warp >> 1) * (kRegion / 4);
     for (int bin = lane; bin < 256; bin += 32) {
       uint32_t sacc = 0;
       for (int k = 0; k < 32; ++k) {
         const int l = (k + lane) & 31;
-        const uint32_t v = tab[bin * 32 + l];
+        const uint32_t v = tab[tab_word(bin, warp, l)];
         sacc += v;
         if (VERIFY && (a.verify & V_PARTIALS)) {
           for (int lv = 0; lv < a.nlev; ++lv)
@@ -252,7 +278,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
 template <bool V, int VPL>
 cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
   auto kern = hist_kernel<V, VPL>;
-  const size_t smem = (size_t)kStages * tile + (size_t)W * 256 * 32 * 4;
+  const size_t smem = (size_t)kStages * tile + (size_t)((W + 1) / 2) * kRegion;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -289,7 +315,10 @@ bool hist_matches(const NestArgs& a, const char** why) {
   if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 512) { *why = "warp static(512)"; return false; }
   if (k->sched != SCHED_STATIC_CHUNK || tile % (512 * W) != 0 || tile > 32768) { *why = "CTA static(tile)"; return false; }
   if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster static(K*tile)"; return false; }
-  if (W > kMaxW || kStages * tile + W * 32768 > 227 * 1024) { *why = "W <= 6 (32 KiB lane tables per warp)"; return false; }
+  if (W > kMaxW || kStages * tile + ((W + 1) / 2) * kRegion > 227 * 1024) {
+    *why = "W <= 6 (64 KiB lane-table region per warp pair)";
+    return false;
+  }
   return true;
 }
 
