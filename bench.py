@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "elements/s and HBM GB/s (% of peak) for nested reductions at 1/2/4/8 B200"
 NOMINAL_HBM_GBS = 8000.0
-RED_SHARED_PEAK_UPS = 5.764e12  # red.shared.add.u32, lane-private (profiles/r01_red_shared_peak.txt)
+RED_SHARED_PEAK_UPS = 8.785e12  # red.shared.add.u32, lane-private (profiles/r01_red_shared_peak.txt)
 L2_BYTES = 126 * 2 ** 20
 
 
