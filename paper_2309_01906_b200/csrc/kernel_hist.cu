@@ -32,7 +32,12 @@
 namespace hpar {
 namespace {
 
-constexpr int kStages = 5;  // 5 x 16 KiB in flight per CTA next to 4 x 32 KiB lane tables
+constexpr int kStages = 5;  // TMA ring stages at most (fewer when the lane tables leave less room)
+constexpr int kSmemBudget = 227 * 1024 - 8 * 1024;  // dynamic smem next to the static arrays
+__host__ __device__ __forceinline__ int ring_stages(int W, int tile) {
+  const int room = (kSmemBudget - ((W + 1) / 2) * 65536) / tile;
+  return room < kStages ? room : kStages;
+}
 constexpr int kMaxW = 6;  // 3 x 64 KiB lane-table regions + the ring fit in 227 KiB
 constexpr int kRegion = 65536;  // lane tables of a warp pair
 
@@ -46,7 +51,7 @@ __device__ __forceinline__ void inc_shared(uint32_t addr) {
 
 // VPL: 16-byte vectors per lane per tile (tile == 512*W*VPL), 0 = generic
 template <bool VERIFY, int VPL>
-__global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ NestArgs a, int W, int tile) {
+__global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ NestArgs a, int W, int tile, int nst) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t wbins[kMaxW][256];
@@ -71,7 +76,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
 
   for (int i = threadIdx.x; i < (int)(table_bytes(W) / 4); i += blockDim.x) counts[i] = 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], W);
     }
@@ -85,13 +90,13 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
       int s = 0;
       uint32_t ph = 0;
       for (int64_t j = 0; j < my_tiles; ++j) {
-        if (j >= kStages) mbar_wait(&empty[s], ph ^ 1);
+        if (j >= nst) mbar_wait(&empty[s], ph ^ 1);
         const int64_t base = (j * nblocks + b) * tile;
         const int64_t len = (n - base < tile) ? (n - base) : tile;
         const uint32_t bytes = (uint32_t)(len & ~(int64_t)15);
         mbar_arrive_expect_tx(&full[s], bytes);
         if (bytes) bulk_g2s(ring + (size_t)s * tile, x + base, bytes, &full[s], pol);
-        if (++s == kStages) { s = 0; ph ^= 1; }
+        if (++s == nst) { s = 0; ph ^= 1; }
       }
     }
   } else {
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      if (++s == kStages) { s = 0; ph ^= 1; }
+      if (++s == nst) { s = 0; ph ^= 1; }
     }
    };
     switch (warp >> 1) {
@@ -278,7 +283,8 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
 template <bool V, int VPL>
 cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
   auto kern = hist_kernel<V, VPL>;
-  const size_t smem = (size_t)kStages * tile + (size_t)((W + 1) / 2) * kRegion;
+  const int nst = ring_stages(W, tile);
+  const size_t smem = (size_t)nst * tile + (size_t)((W + 1) / 2) * kRegion;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -293,7 +299,7 @@ cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, W, tile);
+  return cudaLaunchKernelEx(&cfg, kern, a, W, tile, nst);
 }
 
 }  // namespace
@@ -315,7 +321,7 @@ bool hist_matches(const NestArgs& a, const char** why) {
   if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 512) { *why = "warp static(512)"; return false; }
   if (k->sched != SCHED_STATIC_CHUNK || tile % (512 * W) != 0 || tile > 32768) { *why = "CTA static(tile)"; return false; }
   if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster static(K*tile)"; return false; }
-  if (W > kMaxW || kStages * tile + ((W + 1) / 2) * kRegion > 227 * 1024) {
+  if (W > kMaxW || ring_stages((int)W, (int)tile) < 2) {
     *why = "W <= 6 (64 KiB lane-table region per warp pair)";
     return false;
   }
