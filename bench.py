@@ -240,7 +240,9 @@ def run_hpar(args):
         elems_rank = cnt
         host_out_bytes = out.numel() * out.element_size()
     elif kind == "c1":
-        nest = H.Nest(nests.c1_nest(), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+        teams = int(os.environ.get("HPAR_C1_TEAMS", "1024"))  # (knob) 0 = resident clusters x K
+        nest = H.Nest(nests.c1_nest(outer=teams), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
+                      clusters=args.clusters if teams == 0 else 0,
                       flags=H.HPAR_NEST_NODE_FUSED if (args.node == "fused" and comm is not None) else 0)
         b, cnt = nest.shard_range(spec["n0"] * world, rank)
         x = torch.empty(cnt * 1024, dtype=torch.int32, device=dev)
@@ -482,7 +484,9 @@ def oracle_step_fn(config: str, n_elems: int):
         side = int(max(64, min(16386, int(np.sqrt(max(n_elems, 1))))))
         a = gen.gen_f32(gen.SEED_C5, 0, side * side).reshape(side, side)
         return (lambda: G.stencil5_step(a)), side * side, f"ghostmap.stencil5_step (numpy fp32) on {side} x {side}"
-    n = max(1024, n_elems)
+    # the sample is bounded: c1's whole workload is 2^20 elements; c4/c5 at
+    # most 2^28 elements (1 GiB of fp32) per step
+    n = max(1024, min(n_elems, (1 << 20) if config == "c1" else (1 << 28)))
     if config == "c4":
         x = gen.gen_u8(gen.SEED_C4, 0, n)
         return (lambda: O.hist256(x)), n, f"or_hist256 over bytes [0,{n})"
