@@ -131,7 +131,7 @@ __device__ __forceinline__ float max_nan_abs(float m, float v) {  // max(m, |v|)
 }
 
 template <bool VERIFY, bool OUT_F32, int LPL, int D>
-__global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg, int long_min) {
+__global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg, int long_min, int cb) {
   using RT = typename std::conditional<OUT_F32, float, double>::type;
   constexpr int WIN = 32 * LPL;
   extern __shared__ __align__(128) unsigned char seg_dsm[];
@@ -174,12 +174,12 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
   // to D ahead.  Two-level dynamic chunking: a warp takes the next block of
   // its CTA's chunk list from a shared-memory ticket; the warp that opens
   // chunk j claims it from the GPU ticket (CB blocks at a time).
-  const int64_t nchunks = (nblocks + CB - 1) / CB;
+  const int64_t nchunks = (nblocks + cb - 1) / cb;
   auto claim = [&]() -> unsigned long long {
     long long blk = 0;
     if (lane == 0) {
       const unsigned v = atomicAdd(&cs.ctr, 1u);
-      const unsigned j = v / CB, sub = v % CB;
+      const unsigned j = v / (unsigned)cb, sub = v % (unsigned)cb;
       if (sub == 0) {
         cs.sblock[j % NSB] = (long long)atomicAdd(ws.block_ticket, 1ull);
         __threadfence_block();
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
         __threadfence_block();
       }
       const long long g = ((volatile long long*)cs.sblock)[j % NSB];
-      blk = (g < nchunks) ? g * CB + sub : (long long)nblocks + 1;
+      blk = (g < nchunks) ? g * cb + sub : (long long)nblocks + 1;
     }
     return (unsigned long long)__shfl_sync(0xffffffffu, blk, 0);
   };
@@ -719,7 +719,10 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
     static int lmin = -1;
     if (lmin < 0) lmin = getenv("HPAR_SEG_LONG") ? atoi(getenv("HPAR_SEG_LONG")) : (int)LONG;
     if (lmin < (int)LONG) lmin = (int)LONG;  // the queue is sized for rows > LONG
-    return cudaLaunchKernelEx(&cfg, kern, a, ws, dbg, lmin);
+    static int cbk = -1;
+    if (cbk < 0) cbk = getenv("HPAR_SEG_CB") ? atoi(getenv("HPAR_SEG_CB")) : CB;
+    if (cbk < 1) cbk = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, ws, dbg, lmin, cbk);
   };
   // variant: LPL from the nest's lane chunk; ring depth D (HPAR_SEG_D knob)
   const int lpl = device_levels(a).l[1]->chunk;
