@@ -113,6 +113,7 @@ struct WarpSmem {
   int32_t lrange[NL][2];         // the first NL long rows: [start, end) relative to base
   int32_t slot_wr[D];            // window position (relative to base) held by each slot
   uint64_t bar[D];               // ring slot "full" barriers
+  uint64_t bar2[2];              // the two extra slots of the deep segment ring (D == 2)
 };
 static_assert(RB == 256, "the flush gives each lane 8 consecutive rows");
 static_assert(sizeof(WarpSmem<float, 16, 3>) % 16 == 0 && sizeof(WarpSmem<double, 8, 4>) % 16 == 0, "TMA alignment");
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
   if (threadIdx.x == 0) cs.ctr = 0;
   if (threadIdx.x < NSB) cs.tag[threadIdx.x] = 0;
   if (lane < D) mbar_init(&sm.bar[lane], 1);
+  if (lane < 2) mbar_init(&sm.bar2[lane], 1);
   for (int i = lane; i < D * WIN; i += 32) (&sm.ring[0][0])[i] = 0.f;  // defined bytes beyond partial copies
   fence_mbarrier_init_cluster();
   fence_proxy_async_shared();
@@ -217,7 +219,17 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
   // One published long-row segment: its nonzeros stream through the ring
   // (fp32 per lane and window, fp64 across); the row's LAST segment to
   // finish folds the segment partials in ascending order.
-  auto do_segment = [&](unsigned long long q) {
+  // DEEP (after the warp's blocks, D == 2): 4 window slots — the ring plus
+  // the then idle prefix and offsets/results areas — so a segment keeps 3
+  // windows (6 KiB) in flight instead of 1.
+  auto do_segment = [&](unsigned long long q, auto deep_c) {
+    constexpr bool DEEP = decltype(deep_c)::value && D == 2;
+    constexpr int NS = DEEP ? 4 : D;
+    auto slot_ptr = [&](int s) -> float* {
+      if constexpr (DEEP) return s == 0 ? &sm.ring[0][0] : s == 1 ? &sm.ring[1][0] : s == 2 ? (float*)&sm.E[0][0] : (float*)&sm.off[0];
+      else return &sm.ring[s][0];
+    };
+    auto slot_bar = [&](int s) -> uint64_t* { return s < D ? &sm.bar[s] : &sm.bar2[s - D]; };
     long long row = -1, b = 0;
     int len = 0, k = 0, ns = 0;
     if (lane == 0) {
@@ -241,31 +253,37 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     const int64_t e4 = (e + 3) & ~(int64_t)3;
     const int c4 = (int)((e4 < nnz4 ? e4 : nnz4) - sb);  // copied by TMA; beyond: the array's tail
     const int bo = (int)(b - sb);
+    // windows are issued and consumed in order: window i sits at i * WIN and
+    // in slot i % NS (own counters; every slot's barrier parity in `phases`)
+    int ni = 0, nc = 0;
     auto seg_issue = [&](int w) {
-      const int s = (int)(iseq % D);
+      const int s = ni % NS;
       if (lane == 0) {
-        sm.slot_wr[s] = w;
         const int m = (c4 - w < WIN) ? c4 - w : WIN;
         if (m > 0) {
-          mbar_arrive_expect_tx(&sm.bar[s], (uint32_t)m * 4u);
-          bulk_g2s(&sm.ring[s][0], x + sb + w, (uint32_t)m * 4u, &sm.bar[s], pol);
+          mbar_arrive_expect_tx(slot_bar(s), (uint32_t)m * 4u);
+          bulk_g2s(slot_ptr(s), x + sb + w, (uint32_t)m * 4u, slot_bar(s), pol);
         } else {
-          mbar_arrive(&sm.bar[s]);
+          mbar_arrive(slot_bar(s));
         }
       }
-      ++iseq;
+      ++ni;
     };
     int iw = 0;
-    for (int d = 0; d < D && iw < n; ++d, iw += WIN) seg_issue(iw);
+    for (int d = 0; d < NS && iw < n; ++d, iw += WIN) seg_issue(iw);
     double acc = 0.0;
-    while (cseq != iseq) {
-      const int s = ring_wait();
-      const int wr = sm.slot_wr[s];
+    while (nc != ni) {
+      const int s = nc % NS;
+      mbar_wait(slot_bar(s), (phases >> s) & 1u);
+      phases ^= 1u << s;
+      const int wr = nc * WIN;
+      ++nc;
+      const float* slot = slot_ptr(s);
       const int p = wr + LPL * lane;
       float v[LPL];
 #pragma unroll
       for (int j = 0; j < LPL / 4; ++j) {
-        const float4 t = *(const float4*)&sm.ring[s][LPL * lane + 4 * j];
+        const float4 t = *(const float4*)&slot[LPL * lane + 4 * j];
         v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
       }
       if (wr == 0 || wr + WIN > n) {  // segment edges; the array's unaligned tail
@@ -558,7 +576,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
         head = __shfl_sync(0xffffffffu, head, 0);
         if (myq == NONE && head < tail) claim_seg();
         if (myq == NONE || myq >= tail) break;
-        do_segment(myq);
+        do_segment(myq, std::false_type());
         myq = NONE;
       }
     }
@@ -590,7 +608,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     if (myq == NONE && head < tail) claim_seg();
     if (myq != NONE && myq < tail) {
       const unsigned long long t0 = ws.dbg_t ? gtimer() : 0;
-      do_segment(myq);
+      do_segment(myq, std::true_type());  // after the blocks: deep ring
       if (ws.dbg_t) { ++dbg_nseg; dbg_tseg += gtimer() - t0; }
       myq = NONE;
       nap = 32;
