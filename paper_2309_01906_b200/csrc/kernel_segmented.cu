@@ -35,6 +35,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <algorithm>
 #include <type_traits>
 #include "fused_common.cuh"
 
@@ -779,6 +780,14 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
     fprintf(stderr, "seg times (us): start avg %.1f | phase1 end avg %.1f min %.1f max %.1f | exit avg %.1f max %.1f"
             " | phase2 segs/warp %.2f, us/seg %.2f, all-blocks-done seen avg %.1f min %.1f\n",
             st / nwarps, s1 / nwarps, p1min, p1max, s2 / nwarps, (tmax - t0) * 1e-3, nseg / nwarps, tseg / (nseg > 0 ? nseg : 1), tdone / nwarps, tdmin);
+    {  // phase-1 end percentiles
+      double* e1 = (double*)malloc(nwarps * sizeof(double));
+      for (int64_t w = 0; w < nwarps; ++w) e1[w] = (h[6 * w + 1] - t0) * 1e-3;
+      std::sort(e1, e1 + nwarps);
+      fprintf(stderr, "seg phase1 end percentiles (us): p10 %.1f p50 %.1f p90 %.1f p99 %.1f p99.9 %.1f\n", e1[nwarps / 10],
+              e1[nwarps / 2], e1[nwarps * 9 / 10], e1[nwarps * 99 / 100], e1[nwarps * 999 / 1000]);
+      free(e1);
+    }
     free(h);
   }
   return er;
