@@ -499,35 +499,39 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
         if (lane == 31) sm.E[0][32].x = incl;
         __syncwarp();
       }
-      // one lane per row overlapping the window, 32 rows per step
+      // one lane per row overlapping the window, 32 rows per step.  Straight-
+      // line per lane: indices are clamped and results selected, so lanes
+      // past the window's rows compute a discarded value instead of branching.
+      const bool tail_win = wend > lim4;  // the array's unaligned tail is not in the ring
       int r = rcur;
       for (;;) {
         const int i = r + lane;
-        const bool valid = i < nr && sm.off[i] < wend;
+        const int s_ = sm.off[i < nr ? i : nr];
+        const int e_ = sm.off[i + 1 < nr ? i + 1 : nr];
+        const bool valid = i < nr && s_ < wend;
+        // clamped: a long row whose windows were skipped may end before wr
+        const int sc = min(max(s_ - wr, 0), WIN);
+        const int ec = min(max(e_ - wr, sc), WIN);
         double val = 0.0;
-        bool complete = false;
-        if (valid) {
-          const int s_ = sm.off[i], e_ = sm.off[i + 1];
-          // clamped: a long row whose windows were skipped may end before wr
-          const int sc = min(max(s_ - wr, 0), WIN);
-          const int ec = min(max(e_ - wr, sc), WIN);
-          if (exact) {
-            // an odd end / start adds the one value before it (the array's
-            // unaligned tail is not in the ring: read it directly)
-            auto at = [&](int q) -> float { return (wr + q >= lim4) ? x[base + wr + q] : sm.ring[s][q]; };
-            val = (e_even<LPL>(sm, ec & ~1) - e_even<LPL>(sm, sc & ~1)) +
-                  ((double)((ec & 1) ? at(ec - 1) : 0.f) - (double)((sc & 1) ? at(sc - 1) : 0.f));
-          } else {
-            for (int q = sc; q < ec; ++q) val += (double)((wr + q >= lim4) ? x[base + wr + q] : sm.ring[s][q]);
+        if (exact) {
+          // an odd end / start adds the one value before it
+          float ve = sm.ring[s][ec > 0 ? ec - 1 : 0];
+          float vs = sm.ring[s][sc > 0 ? sc - 1 : 0];
+          if (tail_win) {
+            if (ec > 0 && wr + ec - 1 >= lim4) ve = x[base + wr + ec - 1];
+            if (sc > 0 && wr + sc - 1 >= lim4) vs = x[base + wr + sc - 1];
           }
-          if (s_ < wr) val += carry;  // the row open from the previous window
-          complete = e_ <= wend;
-          const bool lg = (sm.lmask[i >> 5] >> (i & 31)) & 1u;
-          if (complete && !lg) sm.res[i] = (RT)val;
-          if constexpr (VERIFY) {
-            if (!lg)
-              for (int q = sc; q < ec; ++q) cover_by(base + wr + q, leaf0 + q / LPL);
-          }
+          val = (e_even<LPL>(sm, ec & ~1) - e_even<LPL>(sm, sc & ~1)) +
+                ((double)((ec & 1) ? ve : 0.f) - (double)((sc & 1) ? vs : 0.f));
+        } else if (valid) {
+          for (int q = sc; q < ec; ++q) val += (double)((wr + q >= lim4) ? x[base + wr + q] : sm.ring[s][q]);
+        }
+        if (s_ < wr) val += carry;  // the row open from the previous window
+        const bool complete = valid && e_ <= wend;
+        if (complete) sm.res[i] = (RT)val;  // a long row's slot is never flushed
+        if constexpr (VERIFY) {
+          if (valid && !((sm.lmask[i >> 5] >> (i & 31)) & 1u))
+            for (int q = sc; q < ec; ++q) cover_by(base + wr + q, leaf0 + q / LPL);
         }
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
         const unsigned cm = __ballot_sync(0xffffffffu, complete);
