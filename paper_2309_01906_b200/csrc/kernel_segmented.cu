@@ -103,11 +103,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 template <typename RT, int LPL, int D>
-struct WarpSmem {
+struct alignas(16) WarpSmem {
   static constexpr int WIN = 32 * LPL;
   float ring[D][WIN];            // window ring (TMA destinations)
-  double2 E[LPL / 4][33];        // window exclusive prefix at even positions q: j = (q % LPL) / 2 in
-                                 // E[j / 2][q / LPL] (.x/.y by j % 2); q = WIN: E[0][32].x
+  double E[32 * (LPL / 2 + 1) + 2];  // window exclusive prefix at even positions q, at
+                                     // q / 2 + q / LPL (one pad per lane: conflict-free)
   int32_t off[RB + 4];           // the block's RB+1 offsets relative to base
   RT res[RB];                    // the block's row results, flushed coalesced
   unsigned int lmask[RB / 32];   // long rows of the block (bit per row): never flushed here
@@ -122,8 +122,7 @@ static_assert(sizeof(WarpSmem<float, 16, 3>) % 16 == 0 && sizeof(WarpSmem<double
 // E at an even window position q (0 <= q <= WIN)
 template <int LPL, typename W>
 __device__ __forceinline__ double e_even(const W& sm, int q) {
-  const int j = (q & (LPL - 1)) >> 1;
-  return (&sm.E[0][0].x)[(j >> 1) * 66 + (q / LPL) * 2 + (j & 1)];
+  return sm.E[(q >> 1) + q / LPL];
 }
 
 __device__ __forceinline__ float max_nan_abs(float m, float v) {  // max(m, |v|), NaN propagating
@@ -227,7 +226,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     constexpr bool DEEP = decltype(deep_c)::value && D == 2;
     constexpr int NS = DEEP ? 4 : D;
     auto slot_ptr = [&](int s) -> float* {
-      if constexpr (DEEP) return s == 0 ? &sm.ring[0][0] : s == 1 ? &sm.ring[1][0] : s == 2 ? (float*)&sm.E[0][0] : (float*)&sm.off[0];
+      if constexpr (DEEP) return s == 0 ? &sm.ring[0][0] : s == 1 ? &sm.ring[1][0] : s == 2 ? (float*)&sm.E[0] : (float*)&sm.off[0];
       else return &sm.ring[s][0];
     };
     auto slot_bar = [&](int s) -> uint64_t* { return s < D ? &sm.bar[s] : &sm.bar2[s - D]; };
@@ -493,10 +492,11 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
         }
         double ex = __shfl_up_sync(0xffffffffu, incl, 1);
         if (lane == 0) ex = 0.0;
-        sm.E[0][lane] = make_double2(ex, ex + c[0]);
+        double* el = &sm.E[(LPL / 2 + 1) * lane];
+        el[0] = ex;
 #pragma unroll
-        for (int k = 1; k < LPL / 4; ++k) sm.E[k][lane] = make_double2(ex + c[2 * k - 1], ex + c[2 * k]);
-        if (lane == 31) sm.E[0][32].x = incl;
+        for (int k = 1; k < LPL / 2; ++k) el[k] = ex + c[k - 1];
+        if (lane == 31) sm.E[32 * (LPL / 2 + 1)] = incl;
         __syncwarp();
       }
       // one lane per row overlapping the window, 32 rows per step.  Straight-
