@@ -31,6 +31,8 @@
 // (or holding Inf/NaN) takes the direct path: each row lane adds its
 // nonzeros in order in fp64.  Row results are staged in shared memory and
 // flushed with coalesced stores.  Results are deterministic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -103,7 +105,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 template <typename RT, int LPL, int D>
-struct alignas(16) WarpSmem {
+struct alignas(1024) WarpSmem {  // 1 KiB: a swizzled TMA box needs 1 KiB-aligned slots
   static constexpr int WIN = 32 * LPL;
   float ring[D][WIN];            // window ring (TMA destinations)
   double E[32 * (LPL / 2 + 1) + 2];  // window exclusive prefix at even positions q, at
@@ -125,19 +127,45 @@ __device__ __forceinline__ double e_even(const W& sm, int q) {
   return sm.E[(q >> 1) + q / LPL];
 }
 
+// index of window position q inside a ring slot (SWZ: 128-byte swizzle)
+template <bool SWZ>
+__device__ __forceinline__ int ring_pos(int q) {
+  if constexpr (SWZ) return (q & ~31) | ((((q >> 2) & 7) ^ ((q >> 5) & 7)) << 2) | (q & 3);
+  else return q;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 seg_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }
+  return fn;
+}
+
 __device__ __forceinline__ float max_nan_abs(float m, float v) {  // max(m, |v|), NaN propagating
   float r;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(m), "f"(fabsf(v)));
   return r;
 }
 
-template <bool VERIFY, bool OUT_F32, int LPL, int D>
-__global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg, int long_min, int cb) {
+// SWZ: block windows arrive as ONE 2-D TMA box [16 rows][32 floats] with
+// the 128-byte swizzle (16-byte chunk c of box row r stored at c ^ (r & 7)),
+// so the lanes' 64-byte runs load without bank conflicts; the array's last
+// partial 32-float row is read directly (limT below).
+template <bool VERIFY, bool OUT_F32, int LPL, int D, bool SWZ = false>
+__global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg, int long_min, int cb,
+                                                               const __grid_constant__ CUtensorMap tmx) {
   using RT = typename std::conditional<OUT_F32, float, double>::type;
   constexpr int WIN = 32 * LPL;
-  extern __shared__ __align__(128) unsigned char seg_dsm[];
+  static_assert(!SWZ || LPL == 16, "swizzled windows: 16 rows of 32 floats");
+  extern __shared__ __align__(128) unsigned char seg_dsm_raw[];
   __shared__ CtaSmem cs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* seg_dsm = seg_dsm_raw + ((1024u - (smem_addr(seg_dsm_raw) & 1023u)) & 1023u);
   WarpSmem<RT, LPL, D>& sm = ((WarpSmem<RT, LPL, D>*)seg_dsm)[warp];
   if (threadIdx.x == 0) cs.ctr = 0;
   if (threadIdx.x < NSB) cs.tag[threadIdx.x] = 0;
@@ -339,7 +367,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     const int nr = (int)((R - r0 < RB) ? (R - r0) : RB);
     // window origin: 64-byte aligned; positions below are 32-bit, relative to
     // it (nnz < 2^31 per rank)
-    const int64_t base = __shfl_sync(0xffffffffu, offr[0], 0) & ~(int64_t)15;
+    const int64_t base = __shfl_sync(0xffffffffu, offr[0], 0) & ~(int64_t)31;  // a whole 128-byte row
 #pragma unroll
     for (int k = 0; k < (RB + 1 + 31) / 32; ++k) {
       const int i = lane + 32 * k;
@@ -395,7 +423,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     // whole 16 bytes of the array; the <= 3 nonzeros beyond are loaded directly
     const int64_t lim64 = nnz_all - base;
     const int lim = lim64 > 0x7FFFFFF0 ? 0x7FFFFFF0 : (int)lim64;
-    const int lim4 = lim & ~3;
+    const int lim4 = SWZ ? lim & ~31 : lim & ~3;  // positions past lim4 are read directly
     const int p1c = ((p1 + 3) & ~3) < lim4 ? ((p1 + 3) & ~3) : lim4;
     int li = 0;  // issuer's cursor over the long-row list
     auto skip = [&](int w) -> int {  // first window at or after w not inside a long row
@@ -415,12 +443,20 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       const int s = (int)(iseq % D);
       if (lane == 0) {
         sm.slot_wr[s] = w;
-        const int n = (p1c - w < WIN) ? p1c - w : WIN;
-        if (n > 0) {
-          mbar_arrive_expect_tx(&sm.bar[s], (uint32_t)n * 4u);
-          bulk_g2s(&sm.ring[s][0], x + base + w, (uint32_t)n * 4u, &sm.bar[s], pol);
+        if constexpr (SWZ) {  // rows past the array's last whole row arrive as zeros
+          mbar_arrive_expect_tx(&sm.bar[s], (uint32_t)WIN * 4u);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+                  "r"(smem_addr(&sm.ring[s][0])), "l"(&tmx), "r"(0), "r"((int)((base + w) >> 5)), "r"(smem_addr(&sm.bar[s]))
+              : "memory");
         } else {
-          mbar_arrive(&sm.bar[s]);
+          const int n = (p1c - w < WIN) ? p1c - w : WIN;
+          if (n > 0) {
+            mbar_arrive_expect_tx(&sm.bar[s], (uint32_t)n * 4u);
+            bulk_g2s(&sm.ring[s][0], x + base + w, (uint32_t)n * 4u, &sm.bar[s], pol);
+          } else {
+            mbar_arrive(&sm.bar[s]);
+          }
         }
       }
       ++iseq;
@@ -443,7 +479,10 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       float v[LPL];
 #pragma unroll
       for (int j = 0; j < LPL / 4; ++j) {
-        const float4 t = *(const float4*)&sm.ring[s][LPL * lane + 4 * j];
+        // SWZ: lane l's run is box row l / 2, chunks (l & 1) * 4 + j, stored
+        // at chunk ^ (row & 7)
+        const int off4 = SWZ ? (lane >> 1) * 32 + ((((lane & 1) * 4 + j) ^ ((lane >> 1) & 7)) << 2) : LPL * lane + 4 * j;
+        const float4 t = *(const float4*)&sm.ring[s][off4];
         v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
       }
       // Positions outside [p0, p1) hold neighbours' (or stale) values: no row
@@ -515,8 +554,8 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
         double val = 0.0;
         if (exact) {
           // an odd end / start adds the one value before it
-          float ve = sm.ring[s][ec > 0 ? ec - 1 : 0];
-          float vs = sm.ring[s][sc > 0 ? sc - 1 : 0];
+          float ve = sm.ring[s][ring_pos<SWZ>(ec > 0 ? ec - 1 : 0)];
+          float vs = sm.ring[s][ring_pos<SWZ>(sc > 0 ? sc - 1 : 0)];
           if (tail_win) {
             if (ec > 0 && wr + ec - 1 >= lim4) ve = x[base + wr + ec - 1];
             if (sc > 0 && wr + sc - 1 >= lim4) vs = x[base + wr + sc - 1];
@@ -524,7 +563,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
           val = (e_even<LPL>(sm, ec & ~1) - e_even<LPL>(sm, sc & ~1)) +
                 ((double)((ec & 1) ? ve : 0.f) - (double)((sc & 1) ? vs : 0.f));
         } else if (valid) {
-          for (int q = sc; q < ec; ++q) val += (double)((wr + q >= lim4) ? x[base + wr + q] : sm.ring[s][q]);
+          for (int q = sc; q < ec; ++q) val += (double)((wr + q >= lim4) ? x[base + wr + q] : sm.ring[s][ring_pos<SWZ>(q)]);
         }
         if (s_ < wr) val += carry;  // the row open from the previous window
         const bool complete = valid && e_ <= wend;
@@ -726,8 +765,37 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool f32 = a.out_dtype == DT_F32;
+  // the values as a [nnz / 32][32] fp32 tensor for the swizzled window boxes
+  // (the last partial row is read directly by the kernel)
+  static CUtensorMap tmx;
+  static const void* tmx_ptr = nullptr;
+  static int64_t tmx_rows = -1;
+  bool tmx_ok = false;
+  {
+    const int64_t rows32 = a.n1 / 32;
+    if (rows32 >= 1 && rows32 < (1ll << 31) && ((uintptr_t)a.in & 15) == 0) {
+      if (tmx_ptr == a.in && tmx_rows == rows32) {
+        tmx_ok = true;
+      } else if (PFN_cuTensorMapEncodeTiled_v12000 enc = seg_encode_fn()) {
+        const cuuint64_t dims[2] = {32, (cuuint64_t)rows32};
+        const cuuint64_t strides[1] = {128};
+        const cuuint32_t box[2] = {32, 16};
+        const cuuint32_t estr[2] = {1, 1};
+        if (enc(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)a.in, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+          tmx_ptr = a.in;
+          tmx_rows = rows32;
+          tmx_ok = true;
+        }
+      }
+    }
+  }
+  static int swz_knob = -1;
+  if (swz_knob < 0) swz_knob = getenv("HPAR_SEG_SWZ") ? atoi(getenv("HPAR_SEG_SWZ")) : 1;
+  if (!swz_knob) tmx_ok = false;
   auto pick = [&](auto kern, size_t warp_smem) -> cudaError_t {
-    cfg.dynamicSmemBytes = WARPS * warp_smem;
+    cfg.dynamicSmemBytes = WARPS * warp_smem + 1024;  // + alignment of the 1 KiB-aligned warp areas
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)cfg.dynamicSmemBytes);
     if (e != cudaSuccess) return e;
@@ -745,7 +813,7 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
     static int cbk = -1;
     if (cbk < 0) cbk = getenv("HPAR_SEG_CB") ? atoi(getenv("HPAR_SEG_CB")) : CB;
     if (cbk < 1) cbk = 1;
-    return cudaLaunchKernelEx(&cfg, kern, a, ws, dbg, lmin, cbk);
+    return cudaLaunchKernelEx(&cfg, kern, a, ws, dbg, lmin, cbk, tmx);
   };
   // variant: LPL from the nest's lane chunk; ring depth D (HPAR_SEG_D knob)
   const int lpl = device_levels(a).l[1]->chunk;
@@ -753,6 +821,15 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
   if (dknob < 0) dknob = getenv("HPAR_SEG_D") ? atoi(getenv("HPAR_SEG_D")) : 0;
   auto launch_v = [&](auto lpl_c, auto d_c) -> cudaError_t {
     constexpr int L = decltype(lpl_c)::value, DD = decltype(d_c)::value;
+    if constexpr (L == 16 && DD == 2) {
+      if (tmx_ok) {
+        if (a.verify)
+          return f32 ? pick(segmented_kernel<true, true, L, DD, true>, sizeof(WarpSmem<float, L, DD>))
+                     : pick(segmented_kernel<true, false, L, DD, true>, sizeof(WarpSmem<double, L, DD>));
+        return f32 ? pick(segmented_kernel<false, true, L, DD, true>, sizeof(WarpSmem<float, L, DD>))
+                   : pick(segmented_kernel<false, false, L, DD, true>, sizeof(WarpSmem<double, L, DD>));
+      }
+    }
     if (a.verify)
       return f32 ? pick(segmented_kernel<true, true, L, DD>, sizeof(WarpSmem<float, L, DD>))
                  : pick(segmented_kernel<true, false, L, DD>, sizeof(WarpSmem<double, L, DD>));
