@@ -307,17 +307,19 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       const int wr = nc * WIN;
       ++nc;
       const float* slot = slot_ptr(s);
-      const int p = wr + LPL * lane;
+      // a segment is one sum: lane l takes float4 chunks l, l + 32, ... of
+      // the window (consecutive lanes, consecutive 16 bytes: no conflicts)
       float v[LPL];
 #pragma unroll
       for (int j = 0; j < LPL / 4; ++j) {
-        const float4 t = *(const float4*)&slot[LPL * lane + 4 * j];
+        const float4 t = *(const float4*)&slot[4 * (32 * j + lane)];
         v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
       }
+      auto pos = [&](int j) { return wr + 4 * (32 * (j >> 2) + lane) + (j & 3); };
       if (wr == 0 || wr + WIN > n) {  // segment edges; the array's unaligned tail
 #pragma unroll
         for (int j = 0; j < LPL; ++j) {
-          const int q2 = p + j;
+          const int q2 = pos(j);
           if (q2 >= c4 && q2 < n) v[j] = x[sb + q2];
           if (q2 < bo || q2 >= n) v[j] = 0.f;
         }
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       acc += (double)((t4[0] + t4[1]) + (t4[2] + t4[3]));
       if constexpr (VERIFY) {
         for (int j = 0; j < LPL; ++j)
-          if (p + j >= bo && p + j < n) cover_by(sb + p + j, leaf);
+          if (pos(j) >= bo && pos(j) < n) cover_by(sb + pos(j), leaf);
       }
       __syncwarp();  // slot s is free again
       if (iw < n) {
