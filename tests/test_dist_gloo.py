@@ -3,7 +3,6 @@ ranges (§8(a) A2), the node-level combine semantics (A9: per-rank results
 folded across ranks equal the whole-node result) and bench.py's
 max-over-ranks timing rule.  The NCCL node level itself runs only on GPUs."""
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -12,17 +11,9 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
-
-
-def _worker(rank, world, port, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _worker(rank, world, store, q):
+    # file rendezvous: no TCP port to race for (127.0.0.1 TCP works too)
+    dist.init_process_group("gloo", init_method=f"file://{store}", rank=rank, world_size=world)
     try:
         import sys
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -69,8 +60,9 @@ def test_two_rank_gloo():
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    import tempfile
+    store = os.path.join(tempfile.mkdtemp(prefix="hpar_gloo_"), "rendezvous")  # a FileStore path
+    procs = [ctx.Process(target=_worker, args=(r, world, store, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in range(world))

@@ -5,7 +5,6 @@ ABI's exchange plan (hpar_map_exchange_plan) with point-to-point send/recv —
 the host logic of hpar_map_exchange, whose NCCL transfer runs only on GPUs.
 After T steps the gathered from-sections equal the sequential stencil."""
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -16,17 +15,9 @@ import torch.multiprocessing as mp
 N, T = 24, 4
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
-
-
-def _worker(rank, world, port, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _worker(rank, world, store, q):
+    # file rendezvous: no TCP port to race for (127.0.0.1 TCP works too)
+    dist.init_process_group("gloo", init_method=f"file://{store}", rank=rank, world_size=world)
     try:
         import sys
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -68,8 +59,9 @@ def test_four_rank_ghost_exchange():
     world = 4
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    import tempfile
+    store = os.path.join(tempfile.mkdtemp(prefix="hpar_gloo_"), "rendezvous")  # a FileStore path
+    procs = [ctx.Process(target=_worker, args=(r, world, store, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in range(world))
