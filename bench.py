@@ -162,7 +162,7 @@ def run_hpar(args):
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     # tuned geometry per config (sweeps in profiles/)
-    tuned = {"c2": (4, 888), "c4": (4, 74)}.get(args.config, (8, 0))
+    tuned = {"c2": (4, 888), "c4": (8, 74)}.get(args.config, (8, 0))
     K = 2
     W = args.warps or tuned[0]
     if args.clusters < 0:

@@ -15,7 +15,13 @@
 //               bin << 8 | (warp & 1) << 7 | lane << 2: ONE byte permute
 //               (PRMT) of the data word with the lane's column gives it, so an
 //               increment is PRMT + one fire-and-forget shared atomic
-//               (red.shared, no return value).
+//               (red.shared, no return value).  With W > 6 consumer warps
+//               (the timed geometry: W = 8) the pairs share R = 2 regions
+//               round robin: pair p uses region p mod R, so a counter sums
+//               the same lane column of W / (2R) warps.  The atomics keep
+//               that exact; the lane and warp levels are then folded inside
+//               the shared counters and not materialised, which is why
+//               lane / warp partials (verify) require private regions.
 //     warp    : sum of its 32 lanes' counters (rotated reads, conflict-free)
 //     CTA     : sum of its warps' bins (ascending warp), bar.sync
 //     cluster : reduce-scatter over DSMEM — CTA k owns bins [256k/K, 256(k+1)/K)
@@ -26,22 +32,22 @@
 // Input stream: producer warp + 1-D TMA bulk ring as in kernel_flat.cu.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <type_traits>
 #include "fused_common.cuh"
 
 namespace hpar {
 namespace {
 
-constexpr int kStages = 5;  // TMA ring stages at most (fewer when the lane tables leave less room)
+constexpr int kStages = 8;  // TMA ring stages at most (fewer when the lane tables leave less room)
 constexpr int kSmemBudget = 227 * 1024 - 8 * 1024;  // dynamic smem next to the static arrays
-__host__ __device__ __forceinline__ int ring_stages(int W, int tile) {
-  const int room = (kSmemBudget - ((W + 1) / 2) * 65536) / tile;
+constexpr int kMaxW = 16;  // consumer warps (private tables: W <= 6, 3 x 64 KiB regions)
+constexpr int kMaxPrivW = 6;
+constexpr int kRegion = 65536;  // lane tables of a warp pair
+__host__ __device__ __forceinline__ int ring_stages(int R, int tile) {
+  const int room = (kSmemBudget - R * kRegion) / tile;
   return room < kStages ? room : kStages;
 }
-constexpr int kMaxW = 6;  // 3 x 64 KiB lane-table regions + the ring fit in 227 KiB
-constexpr int kRegion = 65536;  // lane tables of a warp pair
-
-__device__ __forceinline__ size_t table_bytes(int W) { return (size_t)((W + 1) / 2) * kRegion; }
 // offset of counter (bin, lane) of `warp` inside its pair's region, in words
 __device__ __forceinline__ int tab_word(int bin, int warp, int lane) { return bin * 64 + (warp & 1) * 32 + lane; }
 
@@ -51,10 +57,13 @@ __device__ __forceinline__ void inc_shared(uint32_t addr) {
 
 // VPL: 16-byte vectors per lane per tile (tile == 512*W*VPL), 0 = generic
 template <bool VERIFY, int VPL>
-__global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ NestArgs a, int W, int tile, int nst) {
+// R = lane-table regions: (W+1)/2 (every warp pair its own region: the
+// lane and warp levels materialised, required for VERIFY) or fewer, shared
+// round robin by the pairs (the atomics make sharing exact; the warp level is
+// then folded into the shared counters and not materialised)
+__global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ NestArgs a, int W, int tile, int nst, int R) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  __shared__ uint32_t wbins[kMaxW][256];
   __shared__ uint32_t cbins[256];
   __shared__ int s_flag;
 
@@ -71,10 +80,13 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
   // dynamic smem: the lane-table regions first (their shared addresses are
   // link-time constants, so a region base folds into the atomic's immediate
   // offset), then the TMA ring
-  uint32_t* counts = (uint32_t*)dsm;  // [W/2][256][2][32]
-  unsigned char* ring = dsm + table_bytes(W);
+  uint32_t* counts = (uint32_t*)dsm;  // [R][256][2][32]
+  unsigned char* ring = dsm + (size_t)R * kRegion;
+  // the warp bins reuse the ring once the stream is consumed (nst >= 2 tiles
+  // of >= 512 W bytes >= W x 256 u32)
+  uint32_t(*wbins)[256] = (uint32_t(*)[256])ring;
 
-  for (int i = threadIdx.x; i < (int)(table_bytes(W) / 4); i += blockDim.x) counts[i] = 0;
+  for (int i = threadIdx.x; i < R * (kRegion / 4); i += blockDim.x) counts[i] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
@@ -181,7 +193,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
       if (++s == nst) { s = 0; ph ^= 1; }
     }
    };
-    switch (warp >> 1) {
+    switch ((warp >> 1) % R) {
       case 0: consume(std::integral_constant<int, 0>()); break;
       case 1: consume(std::integral_constant<int, 1>()); break;
       default: consume(std::integral_constant<int, 2>()); break;
@@ -191,8 +203,12 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
   __syncthreads();
 #undef HPAR_INC
   // lane -> warp: warp w sums the 32 lane columns of its table; lane l owns
-  // bins l, l+32, ...; rotated column order keeps the reads conflict-free
-  if (warp < W) {
+  // bins l, l+32, ...; rotated column order keeps the reads conflict-free.
+  // With shared regions the first 2R warps read the (region, column) tables
+  // and the others contribute zero bins.
+  if (warp < W && warp >= 2 * R) {
+    for (int bin = lane; bin < 256; bin += 32) wbins[warp][bin] = 0;
+  } else if (warp < W) {
     const uint32_t* tab = counts + (size_t)(warp >> 1) * (kRegion / 4);
     for (int bin = lane; bin < 256; bin += 32) {
       uint32_t sacc = 0;
@@ -281,10 +297,10 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
 }
 
 template <bool V, int VPL>
-cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
+cudaError_t launch_t(const NestArgs& a, int W, int tile, int R, cudaStream_t s) {
   auto kern = hist_kernel<V, VPL>;
-  const int nst = ring_stages(W, tile);
-  const size_t smem = (size_t)nst * tile + (size_t)((W + 1) / 2) * kRegion;
+  const int nst = ring_stages(R, tile);
+  const size_t smem = (size_t)nst * tile + (size_t)R * kRegion;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -299,10 +315,33 @@ cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, W, tile, nst);
+  return cudaLaunchKernelEx(&cfg, kern, a, W, tile, nst, R);
 }
 
 }  // namespace
+
+// lane or warp partials requested: those levels must be materialised
+static bool inner_partials(const NestArgs& a) {
+  if (!(a.verify & V_PARTIALS)) return false;
+  for (int l = 0; l < a.nlev; ++l)
+    if ((a.lv[l].slast == S_LANE_IN || a.lv[l].slast == S_WARP) && a.partials[l]) return true;
+  return false;
+}
+
+// lane-table regions: private per warp pair when lane / warp partials are
+// requested (or W <= 6 and HPAR_C4_REGIONS unset), else
+// min(HPAR_C4_REGIONS or 2, pairs): two 64 KiB regions leave room for a
+// 5-stage ring of 16 KiB tiles (W = 8: 0.69 ms vs 0.78 ms with one region
+// and 1.25 ms with three, whose ring is 2 stages deep; scripts/sweep_hist2.sh)
+static int hist_regions(const NestArgs& a, int W) {
+  const int pairs = (W + 1) / 2;
+  static int knob = -2;
+  if (knob == -2) knob = getenv("HPAR_C4_REGIONS") ? atoi(getenv("HPAR_C4_REGIONS")) : -1;
+  if (inner_partials(a)) return pairs;
+  int r = knob > 0 ? knob : (W <= kMaxPrivW ? pairs : 2);
+  if (r > 3) r = 3;
+  return r < pairs ? r : pairs;
+}
 
 bool hist_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 1 || a.keyed || a.op != OP_HIST || a.in_dtype != DT_U8) { *why = "flat u8 hist"; return false; }
@@ -321,8 +360,9 @@ bool hist_matches(const NestArgs& a, const char** why) {
   if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 512) { *why = "warp static(512)"; return false; }
   if (k->sched != SCHED_STATIC_CHUNK || tile % (512 * W) != 0 || tile > 32768) { *why = "CTA static(tile)"; return false; }
   if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster static(K*tile)"; return false; }
-  if (W > kMaxW || ring_stages((int)W, (int)tile) < 2) {
-    *why = "W <= 6 (64 KiB lane-table region per warp pair)";
+  const int R = hist_regions(a, (int)W);
+  if (W > kMaxW || (inner_partials(a) && W > kMaxPrivW) || ring_stages(R, (int)tile) < 2) {
+    *why = "W <= 16 (W <= 6 with lane / warp partials: a 64 KiB lane-table region per warp pair)";
     return false;
   }
   return true;
@@ -332,12 +372,23 @@ cudaError_t launch_hist(const NestArgs& a, int W, cudaStream_t s, const char** n
   *name = "hist256_lanepriv_tma";
   const int tile = (int)device_levels(a).l[1]->chunk;
   const int vpl = (tile % (512 * W) == 0) ? tile / (512 * W) : 0;
-  if (a.verify) return vpl == 8 ? launch_t<true, 8>(a, W, tile, s) : launch_t<true, 0>(a, W, tile, s);
+  const int R = hist_regions(a, W);
+  if (a.verify) {
+    switch (vpl) {
+      case 2: return launch_t<true, 2>(a, W, tile, R, s);
+      case 4: return launch_t<true, 4>(a, W, tile, R, s);
+      case 8: return launch_t<true, 8>(a, W, tile, R, s);
+      default: return launch_t<true, 0>(a, W, tile, R, s);
+    }
+  }
   switch (vpl) {
-    case 4: return launch_t<false, 4>(a, W, tile, s);
-    case 8: return launch_t<false, 8>(a, W, tile, s);
-    case 16: return launch_t<false, 16>(a, W, tile, s);
-    default: return launch_t<false, 0>(a, W, tile, s);
+    case 1: return launch_t<false, 1>(a, W, tile, R, s);
+    case 2: return launch_t<false, 2>(a, W, tile, R, s);
+    case 3: return launch_t<false, 3>(a, W, tile, R, s);
+    case 4: return launch_t<false, 4>(a, W, tile, R, s);
+    case 8: return launch_t<false, 8>(a, W, tile, R, s);
+    case 16: return launch_t<false, 16>(a, W, tile, R, s);
+    default: return launch_t<false, 0>(a, W, tile, R, s);
   }
 }
 

@@ -325,6 +325,44 @@ def test_hist_fused_kernel(H, torch_mod, oracle, n):
             compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
 
 
+@pytest.mark.parametrize("W,tile", [(8, 16384), (16, 8192), (12, 12288)])
+def test_hist_shared_regions(H, torch_mod, oracle, W, tile):
+    """W > 6 consumer warps: warp pairs share one lane-table region (the
+    atomics keep it exact; the warp level is folded into the shared counters).
+    Totals, coverage (every byte once, owner = static closed form) and the
+    CTA / cluster / GPU partials vs the oracle; uniform, skewed, all-zero."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c4_nest(K=2, tile=tile)
+    C, K = 3, 2
+    for n in (0, 5, tile * 2 * 7 + 9, 1 << 20):
+        for x in (gen.gen_u8(gen.SEED_C4, 0, n), gen.gen_u8_zipf(gen.SEED_C4, 0, n), np.zeros(n, np.uint8)):
+            res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, coverage=n <= 300000,
+                           partials=False)
+            assert res["kernel"] == "hist256_lanepriv_tma"
+            assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
+            if n <= 300000:
+                assert (res["count"] == 1).all()
+    # outer-level partials (cluster, CTA) with shared regions
+    n = tile * 2 * 5 + 3
+    x = gen.gen_u8(gen.SEED_C4, 1, n)
+    nest = H.Nest(levels, device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.zeros(256, dtype=torch.int64, device="cuda")
+    cl = torch.zeros((C, 256), dtype=torch.int64, device="cuda")
+    cta = torch.zeros((C * K, 256), dtype=torch.int64, device="cuda")
+    parts = [None, cl, cta, None, None]
+    nest.parallel_for_reduce(H.make_desc(xd, out, n0=n, op=H.OP_HIST256, verify=H.VERIFY_PARTIALS, partials=parts))
+    torch.cuda.synchronize()
+    cta_h = cta.cpu().numpy().astype(np.uint64)
+    for b in range(C * K):
+        h = np.zeros(256, dtype=np.uint64)
+        for s in range(b * tile, n, C * K * tile):
+            h += oracle.hist256(x[s:s + tile])
+        assert np.array_equal(cta_h[b], h), f"CTA {b}"
+    assert np.array_equal(cl.cpu().numpy().astype(np.uint64).sum(axis=0), oracle.hist256(x))
+
+
 def _csr_cases():
     off_z = gen.csr_offsets(3000, 40000)
     yield "zipf", off_z
