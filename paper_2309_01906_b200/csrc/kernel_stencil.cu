@@ -52,6 +52,7 @@ struct StParams {
   int tiles_x, tiles_y, ntiles;
   int64_t gr0, gc0;   // global coordinates of local (0, 0) = to.off
   int64_t R, C;       // parent extents
+  int dbg;            // (timing knob HPAR_ST_DEBUG) bit 1: no ghost ring in the box, bit 2: no stores -- results wrong
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
@@ -94,8 +95,8 @@ __global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant
   // traffic; walking column strips per CTA measured 35% slower)
   auto issue = [&](int t, int s) {
     const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
-    mbar_arrive_expect_tx(&bar[s], (uint32_t)(BY * BX * 4));
-    tma_load_2d(st_smem + s * STAGE, &tmap, p.ca0 + tx * TX - 4, p.fr0 + ty * TY - 1, &bar[s]);
+    mbar_arrive_expect_tx(&bar[s], (p.dbg & 1) ? (uint32_t)(TY * TX * 4) : (uint32_t)(BY * BX * 4));
+    tma_load_2d(st_smem + s * STAGE, &tmap, p.ca0 + tx * TX - ((p.dbg & 1) ? 0 : 4), p.fr0 + ty * TY - ((p.dbg & 1) ? 0 : 1), &bar[s]);
   };
   int it = 0;
   if (tid == 0 && (int)blockIdx.x < p.ntiles) issue(blockIdx.x, 0);
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant
         o.y = avg5(cr.y, nr.y, sr.y, cr.x, cr.z);
         o.z = avg5(cr.z, nr.z, sr.z, cr.y, cr.w);
         o.w = avg5(cr.w, nr.w, sr.w, cr.z, right);
-        __stcs((float4*)dst, o);
+        if (!(p.dbg & 2)) __stcs((float4*)dst, o);
         dst += p.ld;
         nr = cr;
         cr = sr;
@@ -228,7 +229,9 @@ cudaError_t launch_stencil5(const hpar_stencil_desc& d, int device, int sm_count
   if (ty_knob < 0) ty_knob = getenv("HPAR_ST_TY") ? atoi(getenv("HPAR_ST_TY")) : 64;
   if (l2p < 0) l2p = getenv("HPAR_ST_L2P") ? atoi(getenv("HPAR_ST_L2P")) : 256;
   const int TYv = (ty_knob == 64) ? 64 : (ty_knob == 16 ? 16 : 32);
-  const cuuint32_t box[2] = {BX, (cuuint32_t)(TYv + 2)};
+  static int dbg = -1;
+  if (dbg < 0) dbg = getenv("HPAR_ST_DEBUG") ? atoi(getenv("HPAR_ST_DEBUG")) : 0;
+  const cuuint32_t box[2] = {(dbg & 1) ? (cuuint32_t)TX : (cuuint32_t)BX, (cuuint32_t)(TYv + ((dbg & 1) ? 0 : 2))};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)d.in, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -252,6 +255,7 @@ cudaError_t launch_stencil5(const hpar_stencil_desc& d, int device, int sm_count
   p.gc0 = d.to.off[1];
   p.R = d.extent[0];
   p.C = d.extent[1];
+  p.dbg = dbg;
   (void)device;
   static int nst_knob = -1;
   if (nst_knob < 0) nst_knob = getenv("HPAR_ST_NST") ? atoi(getenv("HPAR_ST_NST")) : 2;

@@ -62,8 +62,21 @@ def main():
              "Captured with `ncu --set full --clock-control none --import-source on` under gpurun on one B200",
              "(scripts/profile_all.sh), after the same command exited 0 without ncu.  Times are from a",
              "serialised, profiled replay: compare shares, not absolutes.  Bytes are per launch.", ""]
+    # sections of configs not re-captured this time are kept from the existing file
+    sections = {}
+    spath = os.path.join(PROF, f"{rnd}_ncu_summary.md")
+    if os.path.exists(spath):
+        cur = None
+        for ln in open(spath).read().split("\n"):
+            if ln.startswith("## "):
+                cur = ln[3:].split(":")[0]
+                sections[cur] = []
+            if cur is not None:
+                sections[cur].append(ln)
     for spec in sys.argv[2:]:
         cfg, rep = spec.split(":")
+        body = []
+        sections[cfg] = body
         path = os.path.join(OUT, rep + ".ncu-rep")
         if not os.path.exists(path):
             continue
@@ -73,10 +86,10 @@ def main():
         wr = m.get("dram__bytes_write.sum", (0,))[0]
         dur = m.get("gpu__time_duration.sum", (0,))[0]
         traffic[f"{cfg}:{short}"] = int(rd + wr)
-        lines.append(f"## {cfg}: `{name[:110]}`")
-        lines.append("")
-        lines.append("| metric | value |")
-        lines.append("|---|---|")
+        body.append(f"## {cfg}: `{name[:110]}`")
+        body.append("")
+        body.append("| metric | value |")
+        body.append("|---|---|")
         for k, (v, u) in m.items():
             if isinstance(v, float):
                 if u.endswith("byte"):
@@ -85,14 +98,19 @@ def main():
                     v = f"{v * 1e6:,.2f} us"
                 else:
                     v = f"{v:,.2f} {u}"
-            lines.append(f"| {k} | {v} |")
+            body.append(f"| {k} | {v} |")
         if dur:
-            lines.append(f"| DRAM read+write / duration | {(rd + wr) / dur / 1e9:,.0f} GB/s |")
-        lines.append("")
+            body.append(f"| DRAM read+write / duration | {(rd + wr) / dur / 1e9:,.0f} GB/s |")
+        body.append("")
         lc = os.path.join(OUT, f"launches_{cfg}.csv")
         if os.path.exists(lc):
             shutil.copy(lc, os.path.join(PROF, f"{rnd}_launches_{cfg}.csv"))
-    open(os.path.join(PROF, f"{rnd}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
+    for cfg in sorted(sections):
+        body = sections[cfg]
+        while body and body[-1] == "":
+            body.pop()
+        lines += body + [""]
+    open(spath, "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(tpath, "w"), indent=1, sort_keys=True)
     print("\n".join(lines))
 
