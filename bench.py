@@ -182,7 +182,8 @@ def run_hpar(args):
         H.hpar_map_validate(mspec)
         to, fr = H.hpar_map_sections(mspec, rank)
         nest = H.Nest(nests.stencil_nest(), device=local, nccl_comm=comm)
-        ld = (tile + 2 + 3) // 4 * 4
+        lda = int(os.environ.get("HPAR_C6_LDA", "32"))  # row pitch: whole 128-byte lines (knob; 4 = 16 B, 2.5% slower)
+        ld = (tile + 2 + lda - 1) // lda * lda
         x = torch.empty((tile + 2, ld), dtype=torch.float32, device=dev)
         L.hpar_inputs_fill_f32(spec["seed"], rank * x.numel(), x.numel(), x.data_ptr(), sptr)
         out = x.clone()

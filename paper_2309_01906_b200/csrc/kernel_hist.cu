@@ -44,8 +44,10 @@ constexpr int kSmemBudget = 227 * 1024 - 8 * 1024;  // dynamic smem next to the 
 constexpr int kMaxW = 16;  // consumer warps (private tables: W <= 6, 3 x 64 KiB regions)
 constexpr int kMaxPrivW = 6;
 constexpr int kRegion = 65536;  // lane tables of a warp pair
-__host__ __device__ __forceinline__ int ring_stages(int R, int tile) {
-  const int room = (kSmemBudget - R * kRegion) / tile;
+// ring stage stride: a misaligned input copies one more 16-byte granule per tile
+__host__ __device__ __forceinline__ int ring_stride(int tile, uint32_t mis) { return mis ? tile + 16 : tile; }
+__host__ __device__ __forceinline__ int ring_stages(int R, int stride) {
+  const int room = (kSmemBudget - R * kRegion) / stride;
   return room < kStages ? room : kStages;
 }
 // offset of counter (bin, lane) of `warp` inside its pair's region, in words
@@ -75,6 +77,8 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
   const int64_t my_tiles = (b < ntiles) ? (ntiles - 1 - b) / nblocks + 1 : 0;
   const uint8_t* x = (const uint8_t*)a.in;
   const int K = a.K;
+  const uint32_t mis = (uint32_t)((uintptr_t)x & 15);  // misaligned input: byte path (P:252 peel)
+  const int stride = ring_stride(tile, mis);
   const uint32_t crank = cluster_ctarank();
   const int64_t cl = blockIdx.x / K;
   // dynamic smem: the lane-table regions first (their shared addresses are
@@ -105,9 +109,11 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
         if (j >= nst) mbar_wait(&empty[s], ph ^ 1);
         const int64_t base = (j * nblocks + b) * tile;
         const int64_t len = (n - base < tile) ? (n - base) : tile;
-        const uint32_t bytes = (uint32_t)(len & ~(int64_t)15);
+        // misaligned input: copy the enclosing 16-byte granules (never past
+        // the granule of a valid byte); the tile's bytes then start at `mis`
+        const uint32_t bytes = mis ? (uint32_t)((len + mis + 15) & ~(int64_t)15) : (uint32_t)(len & ~(int64_t)15);
         mbar_arrive_expect_tx(&full[s], bytes);
-        if (bytes) bulk_g2s(ring + (size_t)s * tile, x + base, bytes, &full[s], pol);
+        if (bytes) bulk_g2s(ring + (size_t)s * stride, x + base - mis, bytes, &full[s], pol);
         if (++s == nst) { s = 0; ph ^= 1; }
       }
     }
@@ -128,8 +134,8 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
       const int64_t base = (j * nblocks + b) * tile;
       const int64_t len = (n - base < tile) ? (n - base) : tile;
       mbar_wait(&full[s], ph);
-      const unsigned char* st = ring + (size_t)s * tile;
-      if (len == tile && VPL > 0) {
+      const unsigned char* st = ring + (size_t)s * stride + mis;
+      if (len == tile && VPL > 0 && !mis) {
         // all of this lane's vectors of the tile first (ILP over the smem
         // latency), then the increments
         uint4 vv[VPL > 0 ? VPL : 1];
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
               if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
             }
         }
-      } else if (len == tile) {
+      } else if (len == tile && !mis) {
 #pragma unroll 2
         for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
           const uint4 v = ((const uint4*)st)[f];
@@ -175,7 +181,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
           }
         }
       } else {
-        const int64_t in_smem = len & ~(int64_t)15;
+        const int64_t in_smem = mis ? len : (len & ~(int64_t)15);
         for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
           for (int e = 0; e < 16; ++e) {
             const int64_t off = 16 * (int64_t)f + e;
@@ -299,8 +305,9 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
 template <bool V, int VPL>
 cudaError_t launch_t(const NestArgs& a, int W, int tile, int R, cudaStream_t s) {
   auto kern = hist_kernel<V, VPL>;
-  const int nst = ring_stages(R, tile);
-  const size_t smem = (size_t)nst * tile + (size_t)R * kRegion;
+  const int stride = ring_stride(tile, (uint32_t)((uintptr_t)a.in & 15));
+  const int nst = ring_stages(R, stride);
+  const size_t smem = (size_t)nst * stride + (size_t)R * kRegion;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -345,7 +352,6 @@ static int hist_regions(const NestArgs& a, int W) {
 
 bool hist_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 1 || a.keyed || a.op != OP_HIST || a.in_dtype != DT_U8) { *why = "flat u8 hist"; return false; }
-  if (((uintptr_t)a.in & 15) != 0) { *why = "input not 16-byte aligned"; return false; }
   if (a.verify & V_FINGERPRINT) { *why = "fingerprints not produced by the hist kernel"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
   LevelView v = device_levels(a);
@@ -361,7 +367,7 @@ bool hist_matches(const NestArgs& a, const char** why) {
   if (k->sched != SCHED_STATIC_CHUNK || tile % (512 * W) != 0 || tile > 32768) { *why = "CTA static(tile)"; return false; }
   if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster static(K*tile)"; return false; }
   const int R = hist_regions(a, (int)W);
-  if (W > kMaxW || (inner_partials(a) && W > kMaxPrivW) || ring_stages(R, (int)tile) < 2) {
+  if (W > kMaxW || (inner_partials(a) && W > kMaxPrivW) || ring_stages(R, (int)tile + 16) < 2) {
     *why = "W <= 16 (W <= 6 with lane / warp partials: a 64 KiB lane-table region per warp pair)";
     return false;
   }

@@ -45,7 +45,8 @@ namespace hpar {
 namespace {
 
 constexpr int RB = 256;            // rows per block claim
-constexpr int64_t LONG = 4096;     // a row with more nonzeros is split
+constexpr int64_t LONG = 4096;     // a row with more nonzeros is split (default; HPAR_SEG_LONG)
+constexpr int64_t SPLIT_MIN = 256;  // smallest split threshold the queue is sized for
 constexpr int64_t SEG = 8192;      // nonzeros per long-row segment
 constexpr int WARPS = 8;           // warps per CTA (all workers)
 // kernel variants: LPL = nonzeros per lane per window (the nest's lane
@@ -698,7 +699,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
 
 // workspace layout inside the caller-provided buffer
 // upper bound on long-row segments: sum of ceil(len/SEG) over rows longer than LONG
-static int64_t max_segments(int64_t nnz) { return nnz / SEG + nnz / LONG + 64; }
+static int64_t max_segments(int64_t nnz) { return nnz / SEG + nnz / SPLIT_MIN + 64; }
 
 size_t segmented_ws_bytes(int64_t nnz) {
   return 64 * 8 + (size_t)max_segments(nnz) * (sizeof(SegEntry) + 8 + 4) + 4096;
@@ -811,7 +812,7 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
     if (dbg < 0) dbg = getenv("HPAR_SEG_DEBUG") ? atoi(getenv("HPAR_SEG_DEBUG")) : 0;
     static int lmin = -1;
     if (lmin < 0) lmin = getenv("HPAR_SEG_LONG") ? atoi(getenv("HPAR_SEG_LONG")) : (int)LONG;
-    if (lmin < (int)LONG) lmin = (int)LONG;  // the queue is sized for rows > LONG
+    if (lmin < (int)SPLIT_MIN) lmin = (int)SPLIT_MIN;  // the queue is sized for rows > SPLIT_MIN
     static int cbk = -1;
     if (cbk < 0) cbk = getenv("HPAR_SEG_CB") ? atoi(getenv("HPAR_SEG_CB")) : CB;
     if (cbk < 1) cbk = 1;

@@ -18,7 +18,7 @@
 // ((((c + n) + s) + w) + e) / 5 in IEEE fp32 (__fadd_rn, and a division by
 // 5 that is correctly rounded for every input, see div5); parent-boundary
 // cells copy.  Tiles without boundary or section edges take a branch-free
-// path.  2-stage TMA ring per CTA: the next tile's box is in flight while
+// path.  Stores use the default L2 policy (st.global.cs measured 1.5% slower).  2-stage TMA ring per CTA: the next tile's box is in flight while
 // this one is computed.  Measured alternatives (scripts/sweep_stencil.sh):
 // TY = 16 / 32, 3-4 stages, L2 promotion off, per-CTA column-strip walks.
 #include <cuda.h>
@@ -52,7 +52,7 @@ struct StParams {
   int tiles_x, tiles_y, ntiles;
   int64_t gr0, gc0;   // global coordinates of local (0, 0) = to.off
   int64_t R, C;       // parent extents
-  int dbg;            // (timing knob HPAR_ST_DEBUG) bit 1: no ghost ring in the box, bit 2: no stores -- results wrong
+  int dbg;            // (timing knob HPAR_ST_DEBUG) bit 1: no ghost ring in the box, bit 2: no stores -- results wrong; bit 4: streaming (.cs) stores instead of default-policy ones
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant
         o.y = avg5(cr.y, nr.y, sr.y, cr.x, cr.z);
         o.z = avg5(cr.z, nr.z, sr.z, cr.y, cr.w);
         o.w = avg5(cr.w, nr.w, sr.w, cr.z, right);
-        if (!(p.dbg & 2)) __stcs((float4*)dst, o);
+        if (!(p.dbg & 2)) {
+          if (p.dbg & 4) __stcs((float4*)dst, o);
+          else *(float4*)dst = o;
+        }
         dst += p.ld;
         nr = cr;
         cr = sr;
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant
       if (ly < p.fr0 + p.nrows) {
         float* dst = p.out + (int64_t)ly * p.ld + lx;
         if (cols_full && vec_ok) {
-          __stcs((float4*)dst, o);
+          *(float4*)dst = o;
         } else {
           const float ov[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
@@ -181,6 +184,134 @@ __global__ void __launch_bounds__(THREADS) stencil5_kernel(const __grid_constant
       cr = sr;
     }
     __syncthreads();  // stage s is free again
+  }
+}
+
+// Register-streaming variant (HPAR_ST_IMPL=1): work unit = a 128-column
+// strip x RB rows of the from-section; warp static(1) over the units
+// (round robin over all warps of the persistent grid, units numbered band
+// by band so the warps in flight cover contiguous memory); lane static(4)
+// over the strip's columns.  A warp walks down its strip: rows arrive as
+// coalesced 16-byte loads PF rows ahead into a register ring, north / centre
+// / south slide in registers, west / east through SHFL (lanes 0 / 31 load
+// the strip's halo column).  No shared memory: many warps per SM keep the
+// loads in flight.  Same arithmetic and boundary rules as the tiled kernel.
+template <int RB, int PF, int V>
+__global__ void __launch_bounds__(THREADS) stencil5_rows_kernel(const float* __restrict__ in, const StParams p,
+                                                                int strips, int nunits, int len0, int len1) {
+  constexpr int SW = TX * V;  // strip width: V float4 per lane and row, float4 j of lane l at 4 (32 j + l)
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (THREADS / 32);
+  const int64_t gw = (int64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
+  for (int64_t u = gw; u < nunits; u += nw) {
+    const int band = (int)(u / strips), strip = (int)(u - (int64_t)band * strips);
+    const int y0 = p.fr0 + band * RB;
+    const int yend = min(y0 + RB, p.fr0 + p.nrows);
+    const int xs = p.ca0 + strip * SW;
+    const int64_t gy0 = p.gr0 + y0, gxt = p.gc0 + xs;
+    const bool interior = yend == y0 + RB && xs >= p.fc0 && xs + SW <= p.fc0 + p.ncols && y0 >= 1 &&
+                          y0 + RB < len0 && xs >= 1 && xs + SW < len1 && gy0 > 0 && gy0 + RB < p.R && gxt > 0 &&
+                          gxt + SW < p.C;
+    if (interior) {
+      const int lx = xs + 4 * lane;
+      const float* src = in + (int64_t)(y0 - 1) * p.ld + lx;
+      float* dst = p.out + (int64_t)y0 * p.ld + lx;
+      const float* hs = in + (int64_t)y0 * p.ld + (lane == 0 ? xs - 1 : xs + SW);  // halo column of row y0
+      float4 nr[V], cr[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        nr[j] = __ldg((const float4*)(src + TX * j));
+        cr[j] = __ldg((const float4*)(src + p.ld + TX * j));
+      }
+      src += 2 * p.ld;
+#pragma unroll 1
+      for (int r = 0; r < RB; r += PF) {
+        float4 sr[PF][V];
+        float hv[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k)
+#pragma unroll
+          for (int j = 0; j < V; ++j) sr[k][j] = __ldg((const float4*)(src + (int64_t)k * p.ld + TX * j));
+#pragma unroll
+        for (int k = 0; k < PF; ++k) hv[k] = (lane == 0 || lane == 31) ? __ldg(hs + (int64_t)k * p.ld) : 0.f;
+        src += (int64_t)PF * p.ld;
+        hs += (int64_t)PF * p.ld;
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            float left = __shfl_up_sync(0xffffffffu, cr[j].w, 1);
+            float right = __shfl_down_sync(0xffffffffu, cr[j].x, 1);
+            const float lw = j > 0 ? __shfl_sync(0xffffffffu, cr[j > 0 ? j - 1 : 0].w, 31) : hv[k];
+            const float re = j < V - 1 ? __shfl_sync(0xffffffffu, cr[j < V - 1 ? j + 1 : 0].x, 0) : hv[k];
+            if (lane == 0) left = lw;
+            if (lane == 31) right = re;
+            float4 o;
+            o.x = avg5(cr[j].x, nr[j].x, sr[k][j].x, left, cr[j].y);
+            o.y = avg5(cr[j].y, nr[j].y, sr[k][j].y, cr[j].x, cr[j].z);
+            o.z = avg5(cr[j].z, nr[j].z, sr[k][j].z, cr[j].y, cr[j].w);
+            o.w = avg5(cr[j].w, nr[j].w, sr[k][j].w, cr[j].z, right);
+            *(float4*)(dst + TX * j) = o;
+          }
+          dst += p.ld;
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            nr[j] = cr[j];
+            cr[j] = sr[k][j];
+          }
+        }
+      }
+      continue;
+    }
+    for (int sub = 0; sub < V; ++sub) {
+    const int xb = xs + TX * sub;
+    const int lx = xb + 4 * lane;
+    // general unit: predicated loads (cells outside the buffer read as 0 and
+    // are never used), parent-boundary cells copy, writes only inside `from`
+    const bool in_cols = lx + 3 < p.ld;
+    auto ld4 = [&](int y) -> float4 {
+      if (y < 0 || y >= len0 || !in_cols) return make_float4(0.f, 0.f, 0.f, 0.f);
+      return __ldg((const float4*)(in + (int64_t)y * p.ld + lx));
+    };
+    auto ld1 = [&](int y, int x) -> float {
+      if (y < 0 || y >= len0 || x < 0 || x >= (int)p.ld) return 0.f;
+      return __ldg(in + (int64_t)y * p.ld + x);
+    };
+    const int64_t gx0 = p.gc0 + lx;
+    bool colb[4], colin[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      colb[i] = (gx0 + i == 0) || (gx0 + i == p.C - 1);
+      colin[i] = lx + i >= p.fc0 && lx + i < p.fc0 + p.ncols;
+    }
+    float4 nr = ld4(y0 - 1), cr = ld4(y0);
+    for (int y = y0; y < yend; ++y) {
+      const float4 sr = ld4(y + 1);
+      const float hv = ld1(y, lane == 0 ? xb - 1 : xb + TX);
+      float left = __shfl_up_sync(0xffffffffu, cr.w, 1);
+      float right = __shfl_down_sync(0xffffffffu, cr.x, 1);
+      if (lane == 0) left = hv;
+      if (lane == 31) right = hv;
+      const int64_t gy = p.gr0 + y;
+      const bool rowb = (gy == 0) || (gy == p.R - 1);
+      float4 o;
+      o.x = (rowb || colb[0]) ? cr.x : avg5(cr.x, nr.x, sr.x, left, cr.y);
+      o.y = (rowb || colb[1]) ? cr.y : avg5(cr.y, nr.y, sr.y, cr.x, cr.z);
+      o.z = (rowb || colb[2]) ? cr.z : avg5(cr.z, nr.z, sr.z, cr.y, cr.w);
+      o.w = (rowb || colb[3]) ? cr.w : avg5(cr.w, nr.w, sr.w, cr.z, right);
+      float* dst = p.out + (int64_t)y * p.ld + lx;
+      if (colin[0] && colin[3] && in_cols) {
+        *(float4*)dst = o;
+      } else {
+        const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (colin[i]) dst[i] = ov[i];
+      }
+      nr = cr;
+      cr = sr;
+    }
+    }
   }
 }
 
@@ -257,6 +388,32 @@ cudaError_t launch_stencil5(const hpar_stencil_desc& d, int device, int sm_count
   p.C = d.extent[1];
   p.dbg = dbg;
   (void)device;
+  static int impl = -1;
+  if (impl < 0) impl = getenv("HPAR_ST_IMPL") ? atoi(getenv("HPAR_ST_IMPL")) : 0;
+  if (impl == 1 && (d.ld & 3) == 0) {
+    static int vk = -1, pfk = -1, rbk = -1;
+    if (vk < 0) vk = getenv("HPAR_ST_V") ? atoi(getenv("HPAR_ST_V")) : 1;
+    if (pfk < 0) pfk = getenv("HPAR_ST_PF") ? atoi(getenv("HPAR_ST_PF")) : 4;
+    if (rbk < 0) rbk = getenv("HPAR_ST_RB") ? atoi(getenv("HPAR_ST_RB")) : 32;
+    auto go = [&](auto kern, int RB, int V) -> cudaError_t {
+      const int SW = TX * V;
+      const int strips = (p.fc0 + p.ncols - p.ca0 + SW - 1) / SW;
+      const int nunits = ((p.nrows + RB - 1) / RB) * strips;
+      int per_sm = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, 0);
+      if (e != cudaSuccess) return e;
+      int64_t grid = (int64_t)sm_count * (per_sm > 0 ? per_sm : 1);
+      const int64_t need = (nunits + THREADS / 32 - 1) / (THREADS / 32);
+      if (grid > need) grid = need;
+      if (grid < 1) return cudaSuccess;
+      kern<<<(unsigned)grid, THREADS, 0, s>>>(d.in, p, strips, nunits, (int)d.to.len[0], (int)d.to.len[1]);
+      return cudaGetLastError();
+    };
+    if (vk == 4) return pfk >= 2 ? go(stencil5_rows_kernel<32, 2, 4>, 32, 4) : go(stencil5_rows_kernel<32, 1, 4>, 32, 4);
+    if (vk == 2) return pfk >= 4 ? go(stencil5_rows_kernel<32, 4, 2>, 32, 2) : go(stencil5_rows_kernel<32, 2, 2>, 32, 2);
+    if (rbk == 64) return pfk >= 8 ? go(stencil5_rows_kernel<64, 8, 1>, 64, 1) : go(stencil5_rows_kernel<64, 4, 1>, 64, 1);
+    return pfk >= 8 ? go(stencil5_rows_kernel<32, 8, 1>, 32, 1) : go(stencil5_rows_kernel<32, 4, 1>, 32, 1);
+  }
   static int nst_knob = -1;
   if (nst_knob < 0) nst_knob = getenv("HPAR_ST_NST") ? atoi(getenv("HPAR_ST_NST")) : 2;
   if (TYv == 16) return nst_knob >= 4 ? launch_ty<16, 4>(map, p, sm_count, s)

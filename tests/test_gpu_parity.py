@@ -61,7 +61,7 @@ def test_device_generator_matches_numpy(inputs_lib, torch_mod):
 
 # ---------------------------------------------------------------------------
 def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, C=4, K=2, W=4,
-             partials=True, coverage=True, max_inner=0, out_f64=True):
+             partials=True, coverage=True, max_inner=0, out_f64=True, misalign=0):
     nest = H.Nest(levels, device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
     nloops = 2 if (n1 or offsets is not None) else 1
     if offsets is not None:
@@ -69,6 +69,12 @@ def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, 
     else:
         n_iter = n0 * (n1 if nloops == 2 else 1)
     xd = torch.from_numpy(x).cuda()
+    if misalign:  # the input starts `misalign` bytes past a 16-byte boundary
+        assert x.dtype == np.uint8
+        raw = torch.zeros(x.size + 32, dtype=torch.uint8, device="cuda")
+        xd = raw[misalign:misalign + x.size]
+        xd.copy_(torch.from_numpy(x).cuda())
+        assert xd.data_ptr() % 16 == misalign
     fp = x.dtype.kind == "f"
     if op == H.OP_AFFINE:
         out = torch.zeros((n0, 2) if keyed else (2,), dtype=torch.int64, device="cuda")
@@ -322,6 +328,24 @@ def test_hist_fused_kernel(H, torch_mod, oracle, n):
         assert res["kernel"] == "hist256_lanepriv_tma"
         assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
         if n <= 200000:
+            compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
+
+
+@pytest.mark.parametrize("mis", [1, 7, 15])
+def test_hist_misaligned_input(H, torch_mod, oracle, mis):
+    """An input pointer off a 16-byte boundary is not rejected (SURVEY §8(b)
+    alignment): tiles copy their enclosing 16-byte granules and the lanes
+    read bytes at the offset; result, coverage (owner = the nominal static
+    closed form) and every level's partials vs the oracle."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c4_nest(K=2)
+    C, K, W = 3, 2, 4
+    for n in (1, 17, 16384 * 2 * 5 + 7, 200000):
+        for x in (gen.gen_u8(gen.SEED_C4, 0, n), gen.gen_u8_zipf(gen.SEED_C4, 0, n)):
+            res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, misalign=mis)
+            assert res["kernel"] == "hist256_lanepriv_tma"
+            assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
             compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
 
 
