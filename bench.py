@@ -163,7 +163,7 @@ def run_hpar(args):
     sptr = stream.cuda_stream
     # tuned geometry per config (sweeps in profiles/)
     tuned = {"c2": (4, 888), "c4": (8, 74)}.get(args.config, (8, 0))
-    K = 2
+    K = int(os.environ.get("HPAR_K", "2"))  # CTAs per cluster (knob; 2 = tuned)
     W = args.warps or tuned[0]
     if args.clusters < 0:
         args.clusters = tuned[1]
