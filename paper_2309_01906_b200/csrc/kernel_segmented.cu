@@ -41,13 +41,16 @@
 #include <type_traits>
 #include "fused_common.cuh"
 
+#ifndef HPAR_SEG_LEN
+#define HPAR_SEG_LEN 16384
+#endif
 namespace hpar {
 namespace {
 
 constexpr int RB = 256;            // rows per block claim
 constexpr int64_t LONG = 4096;     // a row with more nonzeros is split (default; HPAR_SEG_LONG)
 constexpr int64_t SPLIT_MIN = 256;  // smallest split threshold the queue is sized for
-constexpr int64_t SEG = 8192;      // nonzeros per long-row segment
+constexpr int64_t SEG = HPAR_SEG_LEN;  // nonzeros per long-row segment (16384: -1.5% vs 8192, 32768 +0.5%, 65536 +6%)
 constexpr int WARPS = 8;           // warps per CTA (all workers)
 // kernel variants: LPL = nonzeros per lane per window (the nest's lane
 // static(LPL), 8 or 16), WIN = 32 * LPL per window, D = TMA ring depth

@@ -15,7 +15,7 @@ import os
 from dataclasses import dataclass
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libhpar.so")
+LIB_PATH = os.environ.get("HPAR_LIB") or os.path.join(PKG, "libhpar.so")  # HPAR_LIB: an in-tree experiment build
 
 # ---- enums (include/hpar.h) ---------------------------------------------
 HPAR_OK, HPAR_E_INVALID, HPAR_E_CAPABILITY, HPAR_E_SCHEDULE, HPAR_E_PARTITION = 0, -1, -2, -3, -4

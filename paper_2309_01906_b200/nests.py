@@ -82,7 +82,7 @@ def c3_fast_nest(with_gpu: bool = True, rows_chunk: int = 256, lane_chunk: int =
     over ALL warps of the GPU (cluster..warp collapsed: flags = intersection,
     dynamic and atomic hold); the block's nonzeros (loop 2 = the collapsed
     (row, nonzero) space) static(lane_chunk) over the lanes (8 or 16).  Rows longer than
-    4096 nonzeros are re-bound by length class to dynamic(8192) segments over
+    4096 nonzeros are re-bound by length class to dynamic(16384) segments over
     the warps (kernel_segmented.cu; reading #14)."""
     lv = []
     if with_gpu:
