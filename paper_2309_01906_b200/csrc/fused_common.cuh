@@ -1,6 +1,9 @@
 // fused_common.cuh — helpers shared by the fused (nest-shape specialised)
 // kernels: level-structure matching and the end-of-kernel combine climb.
 #pragma once
+#ifndef HPAR_CLIMB_RELAXED_EXIT
+#define HPAR_CLIMB_RELAXED_EXIT 1
+#endif
 #include "level_primitives.cuh"
 #include "node_fused.cuh"
 #include "plan.h"
@@ -93,7 +96,14 @@ __device__ void fused_total_climb(const NestArgs& a, Acc v, int W, ClimbSmem<Acc
       }
     }
   }
+#if HPAR_CLIMB_RELAXED_EXIT
+  // no data crosses this barrier (the siblings' DSMEM stores were ordered by
+  // the first one): execution-only, no release fence
+  cluster_arrive_relaxed();
+  asm volatile("barrier.cluster.wait;" ::: "memory");
+#else
   cluster_sync_all();  // keep the leader's shared memory alive for its siblings
+#endif
 }
 
 }  // namespace hpar

@@ -31,7 +31,30 @@ __global__ void __launch_bounds__(1024) teams_kernel(const __grid_constant__ Nes
   const In* x = (const In*)a.in;
   const int64_t leaf = (int64_t)a.rank * a.threads_per_gpu + t * NT + j;
   Acc acc = OpT<OP, Acc>::identity();
-  for (int64_t row = row0; row < row0 + nrow; ++row) {
+  // one 16-byte chunk per thread and row (the C1 shape, n1 == 4 NT): a team
+  // with several rows issues up to 8 rows' loads before it combines them
+  const bool one_vec = !VERIFY && sizeof(In) == 4 && chunk == 4 && a.n1 == (int64_t)NT * 4 &&
+                       (((uintptr_t)x) & 15) == 0 && (a.ld & 3) == 0;
+  if (one_vec) {
+    constexpr int G = 8;
+    for (int64_t row = row0; row < row0 + nrow; row += G) {
+      int4 v[G];
+#pragma unroll
+      for (int k = 0; k < G; ++k)
+        v[k] = (row + k < row0 + nrow) ? __ldg((const int4*)(x + (row + k) * a.ld) + j) : make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        if (row + k < row0 + nrow) {
+          const In* e = (const In*)&v[k];
+          acc = OpT<OP, Acc>::combine(acc, (Acc)e[0]);
+          acc = OpT<OP, Acc>::combine(acc, (Acc)e[1]);
+          acc = OpT<OP, Acc>::combine(acc, (Acc)e[2]);
+          acc = OpT<OP, Acc>::combine(acc, (Acc)e[3]);
+        }
+      }
+    }
+  }
+  for (int64_t row = one_vec ? row0 + nrow : row0; row < row0 + nrow; ++row) {
     const In* xr = x + row * a.ld;
     for (int64_t base = (int64_t)j * chunk; base < a.n1; base += (int64_t)NT * chunk) {
       const int64_t end = (base + chunk < a.n1) ? base + chunk : a.n1;

@@ -12,6 +12,9 @@
 // operand (§8(c) reading #4), so non-commutative associative ops fold in
 // ascending task order and sums are run-to-run deterministic.
 #pragma once
+#ifndef HPAR_TICKET_ACQREL
+#define HPAR_TICKET_ACQREL 1
+#endif
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include "plan.h"
@@ -302,10 +305,18 @@ __device__ __forceinline__ bool grid_arrive(Acc my, Acc* partials, unsigned int*
                                             int* s_flag) {
   if (threadIdx.x == 0) {
     partials[c] = my;
+#if HPAR_TICKET_ACQREL
+    // one acq_rel RMW: releases this partial, acquires the others' for the
+    // last arriver (its CTA reads them after the bar.sync below)
+    unsigned int t;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(ticket) : "memory");
+    *s_flag = (t == (unsigned int)(C - 1)) ? 1 : 0;
+#else
     __threadfence();
     unsigned int t = atomicAdd(ticket, 1u);
     *s_flag = (t == (unsigned int)(C - 1)) ? 1 : 0;
     if (*s_flag) __threadfence();
+#endif
   }
   __syncthreads();
   return *s_flag != 0;
