@@ -632,10 +632,8 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     }
   }
 
-  if (lane == 0) {
-    __threadfence();
-    atomicAdd(ws.blocks_done, my_blocks);
-  }
+  if (lane == 0)  // release: this warp's queue entries are visible before its blocks count
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ws.blocks_done), "l"(my_blocks) : "memory");
 
   if (ws.dbg_t && lane == 0) ws.dbg_t[6 * gwarp + 1] = gtimer();
   // ------------------------------- phase 2: the remaining long-row segments ----
@@ -650,7 +648,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     if (lane == 0) {
       tail = *(volatile unsigned long long*)ws.q_tail;
       head = *(volatile unsigned long long*)ws.q_head;
-      done = *(volatile unsigned long long*)ws.blocks_done;
+      done = (unsigned long long)ld_acquire_s64((const long long*)ws.blocks_done);
     }
     tail = __shfl_sync(0xffffffffu, tail, 0);
     head = __shfl_sync(0xffffffffu, head, 0);
@@ -666,8 +664,8 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     }
     if ((int64_t)done >= nblocks) {
       if (ws.dbg_t && !dbg_tdone) dbg_tdone = gtimer();
-      // every entry is published before blocks_done counts its block
-      __threadfence();
+      // every entry is published before blocks_done counts its block (the
+      // acquire above orders these re-reads after it)
       if (lane == 0) {
         tail = *(volatile unsigned long long*)ws.q_tail;
         head = *(volatile unsigned long long*)ws.q_head;
@@ -685,8 +683,8 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
   if (ws.dbg_t && lane == 0) { ws.dbg_t[6 * gwarp + 3] = dbg_nseg; ws.dbg_t[6 * gwarp + 4] = dbg_tseg; ws.dbg_t[6 * gwarp + 5] = dbg_tdone; }
   // --------------------------------------------- exit: last warp resets ----
   if (lane == 0) {
-    __threadfence();
-    const unsigned long long w = atomicAdd(ws.warps_done, 1ull);
+    unsigned long long w;  // acq_rel: the last warp sees every warp's counter updates before it resets them
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(w) : "l"(ws.warps_done) : "memory");
     if ((int64_t)w == (int64_t)gridDim.x * WARPS - 1) {
       *ws.block_ticket = 0ull;
       *ws.q_tail = 0ull;
