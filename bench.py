@@ -318,6 +318,11 @@ def run_hpar(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms = float(t.item())
+    # whole-job HBM rate: every rank's algorithmic bytes / the slowest rank's time
+    tb = torch.tensor([float(alg_bytes)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tb)
+    bytes_all = float(tb.item())
     elems_total = elems_rank * world if spec["scaling"] == "weak" else spec["n0"] * (1024 if kind == "c1" else 1)
     if spec["scaling"] == "strong":
         elems_total = spec.get("elems_total", spec["n0"])
@@ -373,8 +378,10 @@ def run_hpar(args):
                    "geometry": {"C": nest.info().C, "K": K, "W": W},
                    "node_level": ("in-kernel (NCCL LSA)" if args.node == "fused" else "ncclAllReduce")
                    if world > 1 and kind in ("flat", "hist", "c1") else None},
-        "hbm_gbs": achieved * (world if spec["scaling"] == "weak" else 1) if False else achieved,
+        "hbm_gbs": achieved,  # this rank's kernel, algorithmic bytes / device time
         "pct_of_8tbs": achieved / NOMINAL_HBM_GBS,
+        "hbm_gbs_all_gpus": bytes_all / (step_ms * 1e-3) / 1e9,
+        "pct_of_aggregate_peak": bytes_all / (step_ms * 1e-3) / 1e9 / (measured_peak()[0] * world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": kernel,
                      "algorithmic_bytes_per_launch": int(alg_bytes)},
@@ -395,9 +402,30 @@ def run_hpar(args):
 
 
 # ------------------------------------------------------ CPU oracle legs ---
+def host_cpu() -> dict:
+    """The box's CPU model and logical core count (reported next
+    to the oracle's one-core timing)."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_cores": os.cpu_count()}
+
+
 def cpu_baseline(config: str, budget_s: float = 10.0, samples: int = 1):
     """Time the oracle (plain sequential C, one core) on a bounded sample of
-    the workload; returns elements/s and what was sampled."""
+    the workload; returns elements/s, what was sampled and the host CPU."""
+    r = _cpu_baseline(config, budget_s)
+    if r is not None:
+        r.update(host_cpu())
+    return r
+
+
+def _cpu_baseline(config: str, budget_s: float = 10.0):
     import numpy as np
 
     from inputs import gen
@@ -528,7 +556,7 @@ def run_reference(args):
         "config": {"workload": spec["workload"],
                    "kernel": "oracle (CPU, numpy fp32)" if args.config == "c6" else "oracle (CPU, sequential C)"},
         "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{what} per step, {args.steps} timed steps, {dt:.1f} s"},
+                         "sample": f"{what} per step, {args.steps} timed steps, {dt:.1f} s", **host_cpu()},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
