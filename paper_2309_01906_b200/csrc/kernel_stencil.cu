@@ -18,9 +18,13 @@
 // ((((c + n) + s) + w) + e) / 5 in IEEE fp32 (__fadd_rn, and a division by
 // 5 that is correctly rounded for every input, see div5); parent-boundary
 // cells copy.  Tiles without boundary or section edges take a branch-free
-// path.  Stores use the default L2 policy (st.global.cs measured 1.5% slower).  2-stage TMA ring per CTA: the next tile's box is in flight while
-// this one is computed.  Measured alternatives (scripts/sweep_stencil.sh):
-// TY = 16 / 32, 3-4 stages, L2 promotion off, per-CTA column-strip walks.
+// path.  Stores use the default L2 policy (st.global.cs measured 1.5% slower).  4-stage TMA ring and ONE CTA per SM (the ring's 144 KiB
+// leaves room for no second CTA): three boxes are in flight while one is
+// computed.  148 deep read streams beat 444 shallow ones (3 CTAs x 2
+// stages: 0.411 vs 0.343 ms; an L2 prefetch of boxes further ahead made it
+// slower still): the 2-D box rows land on DRAM pages more orderly.
+// Measured alternatives (scripts/sweep_stencil*.sh): TY = 16 / 32 / 128,
+// 2-6 stages, 1-3 CTAs per SM, L2 promotion off, per-CTA column strips.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -341,6 +345,7 @@ cudaError_t launch_ty(const CUtensorMap& map, const StParams& p0, int sm_count, 
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stencil5_kernel<TY, NST>, THREADS, smem);
   if (e != cudaSuccess) return e;
   int grid = sm_count * (per_sm > 0 ? per_sm : 1);
+  if (const char* g = getenv("HPAR_ST_CPS")) grid = sm_count * atoi(g);  // (experiment) CTAs per SM
   if (grid > p.ntiles) grid = p.ntiles;
   if (grid < 1) return cudaSuccess;
   stencil5_kernel<TY, NST><<<grid, THREADS, smem, s>>>(map, p);
@@ -414,11 +419,15 @@ cudaError_t launch_stencil5(const hpar_stencil_desc& d, int device, int sm_count
     if (rbk == 64) return pfk >= 8 ? go(stencil5_rows_kernel<64, 8, 1>, 64, 1) : go(stencil5_rows_kernel<64, 4, 1>, 64, 1);
     return pfk >= 8 ? go(stencil5_rows_kernel<32, 8, 1>, 32, 1) : go(stencil5_rows_kernel<32, 4, 1>, 32, 1);
   }
+  // ring depth: TY = 64 takes 4 stages (144 KiB: one CTA per SM — fewer, deeper
+  // read streams; 3 CTAs x 2 stages measured 0.411 vs 0.343 ms)
   static int nst_knob = -1;
-  if (nst_knob < 0) nst_knob = getenv("HPAR_ST_NST") ? atoi(getenv("HPAR_ST_NST")) : 2;
+  if (nst_knob < 0) nst_knob = getenv("HPAR_ST_NST") ? atoi(getenv("HPAR_ST_NST")) : (TYv == 64 ? 4 : 2);
   if (TYv == 16) return nst_knob >= 4 ? launch_ty<16, 4>(map, p, sm_count, s)
                                       : (nst_knob == 3 ? launch_ty<16, 3>(map, p, sm_count, s) : launch_ty<16, 2>(map, p, sm_count, s));
-  if (TYv == 64) return launch_ty<64, 2>(map, p, sm_count, s);
+  if (TYv == 64)
+    return nst_knob >= 4 ? launch_ty<64, 4>(map, p, sm_count, s)
+         : nst_knob == 3 ? launch_ty<64, 3>(map, p, sm_count, s) : launch_ty<64, 2>(map, p, sm_count, s);
   return nst_knob >= 4 ? launch_ty<32, 4>(map, p, sm_count, s)
                        : (nst_knob == 3 ? launch_ty<32, 3>(map, p, sm_count, s) : launch_ty<32, 2>(map, p, sm_count, s));
 }
