@@ -27,7 +27,10 @@
 // carry of a row open from the previous window.  Those differences are
 // EXACT when the window's nonzero magnitudes span at most EXACT_BINADES
 // binades: every value is then a multiple of the smallest one's ulp and each
-// prefix sum of <= 512 of them fits 53 bits.  A window failing that guard
+// prefix sum of <= 512 of them fits 53 bits.  The guard takes min |v| over
+// the whole window as a float, so an explicit zero (or the zero fill past
+// the array end) counts as binade 0 and sends the window to the direct path
+// (conservative; -2.7% time against skipping zeros, same box).  A window failing that guard
 // (or holding Inf/NaN) takes the direct path: each row lane adds its
 // nonzeros in order in fp64.  Row results are staged in shared memory and
 // flushed with coalesced stores.  Results are deterministic.
@@ -43,6 +46,9 @@
 
 #ifndef HPAR_SEG_LEN
 #define HPAR_SEG_LEN 16384
+#endif
+#ifndef HPAR_SEG_FMIN
+#define HPAR_SEG_FMIN 1
 #endif
 namespace hpar {
 namespace {
@@ -505,6 +511,20 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       }
       // exactness guard: binade span of the window's nonzero magnitudes
       float amax = 0.f;
+#if HPAR_SEG_FMIN
+      // min |v| as a float (3-input FMNMX): a zero makes emin = 0, so a window
+      // holding an explicit zero takes the in-order path (CSR values are
+      // nonzeros; the exact path stays exact either way)
+      float amin = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int k = 0; k < LPL; ++k) {
+        amax = max_nan_abs(amax, v[k]);
+        amin = fminf(amin, fabsf(v[k]));
+      }
+      const unsigned gmax = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));
+      const unsigned gmin = __reduce_min_sync(0xffffffffu, __float_as_uint(amin));
+      const int emax = (int)(gmax >> 23), emin = (int)(gmin >> 23);
+#else
       unsigned umin = 0xFFFFFFFFu;
 #pragma unroll
       for (int k = 0; k < LPL; ++k) {
@@ -515,6 +535,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       const unsigned gmax = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));
       const unsigned gmin = __reduce_min_sync(0xffffffffu, umin);
       const int emax = (int)(gmax >> 23), emin = (int)((gmin + 1u) >> 24);
+#endif
       const bool exact = emax < 255 && emax - emin <= EXACT_BINADES;
       if (exact) {
         // lane-local prefix at even positions: pair sums, then their prefix
