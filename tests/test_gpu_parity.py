@@ -597,3 +597,41 @@ def test_segmented_fuzz(H, torch_mod, oracle, seed):
         assert_rel(out.cpu().numpy(), want)
     if nnz:
         assert (count.cpu().numpy()[:nnz] == 1).all()
+
+
+@pytest.mark.parametrize("values", ["zeros_normal", "zeros_tiny", "subnormal_only", "zero_rows"])
+def test_segmented_explicit_zeros(H, torch_mod, oracle, values):
+    """Explicit zeros and subnormals in the CSR values (DESIGN reading on the
+    C3 exactness guard): a window's min |v| is taken over all its values, so a
+    zero counts as binade 0 — windows holding zeros among normal values take
+    the in-order fp64 path, windows of zeros and values below 2^-106 (binades
+    <= 20) stay on the exact prefix path.  Both must match the oracle's fp64
+    segment sums within 1e-5, rows of zeros exactly 0."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    rng = np.random.default_rng(77)
+    rows = 3000
+    lens = np.where(rng.random(rows) < 0.02, rng.integers(4097, 20000, rows), rng.geometric(0.08, rows))
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(off[-1])
+    v = gen.gen_f32(gen.SEED_C3, 0, nnz)
+    zero = rng.random(nnz) < 0.3
+    if values == "zeros_normal":
+        v = np.where(zero, 0.0, v).astype(np.float32)
+    elif values == "zeros_tiny":
+        tiny = np.ldexp(rng.random(nnz) + 0.5, rng.integers(-150, -107, nnz)).astype(np.float32)
+        v = np.where(zero, 0.0, tiny).astype(np.float32)
+    elif values == "subnormal_only":
+        v = (rng.integers(1, 1 << 23, nnz).astype(np.uint32)).view(np.float32).copy()
+    else:  # every third row all zeros, the rest recipe values
+        rz = np.repeat(np.arange(rows) % 3 == 0, lens)
+        v = np.where(rz, 0.0, v).astype(np.float32)
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=4)
+    xd = torch.from_numpy(v).cuda()
+    offd = torch.from_numpy(off).cuda()
+    out = torch.full((rows,), -1.0, dtype=torch.float64, device="cuda")
+    d = H.make_desc(xd, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd, out_dtype=H.F64)
+    nest.parallel_for_reduce(d)
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "segmented_csr"
+    assert_rel(out.cpu().numpy(), oracle.segsum_f32(v, off))
