@@ -349,12 +349,23 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       }
     }
     acc = warp_fold<OP_SUM>(acc);
+    unsigned t = 0;
     if (lane == 0) {
       __stcg(&ws.partials[q], acc);
-      const unsigned t = atom_add_acq_rel_u32(&ws.tickets[pb], 1u);  // release my partial
-      if ((int)t == ns - 1) {  // last segment of the row: ordered fold (acquired)
-        double tot = 0.0;
-        for (int j = 0; j < ns; ++j) tot += __ldcg(&ws.partials[pb + j]);
+      t = atom_add_acq_rel_u32(&ws.tickets[pb], 1u);  // release my partial
+    }
+    if ((int)__shfl_sync(0xffffffffu, t, 0) == ns - 1) {
+      // last segment of the row: the ordered fold, ascending from 0 as a
+      // sequential loop would add, but the partials are loaded 32 at a time
+      // by the lanes (one L2 round trip per 32 instead of one per partial)
+      __threadfence();  // every lane's loads after lane 0's acquire
+      double tot = 0.0;
+      for (int j0 = 0; j0 < ns; j0 += 32) {
+        const double pj = (j0 + lane < ns) ? __ldcg(&ws.partials[pb + j0 + lane]) : 0.0;
+        const int m = (ns - j0 < 32) ? ns - j0 : 32;
+        for (int l = 0; l < m; ++l) tot += __shfl_sync(0xffffffffu, pj, l);
+      }
+      if (lane == 0) {
         write_row(row, tot);
         ws.tickets[pb] = 0u;
       }
