@@ -23,6 +23,8 @@
  *      PAPER P:83-85 "on each level, one of the tasks collects the results
  *      from all sibling tasks").
  *   4. Coverage fingerprints (verify protocol).
+ *   5. The owner of one iteration of a flat nest (own() followed for one
+ *      position), for fingerprints at full size (2^32-2^34 iterations).
  *
  * Build: gcc -O2 -std=c99 -fPIC -shared (no -ffast-math, no threads).
  * Nothing here is tuned; clarity over speed.
@@ -555,6 +557,98 @@ uint64_t or_fp_owner(const int64_t* owner, uint64_t begin, int64_t n) {
   uint64_t s = 0;
   for (int64_t e = 0; e < n; ++e) s += or_fp_mix2(begin + (uint64_t)e, (uint64_t)owner[e]);
   return s;
+}
+
+/* ========================================================================
+ * 5. Owner of ONE iteration of a flat nest, without materialising lists
+ *    (needed at 2^32-2^34 iterations, where or_nest_run's per-level lists do
+ *    not fit in host memory).  Same semantics as the nest walk: own() applied
+ *    level by level, outermost first, but followed for one
+ *    position p of the parent's list instead of for all of them:
+ *      static:    the task t whose block [t*q + min(t,r), (t+1)*q + min(t+1,r))
+ *                 holds p; p's position in t's list is p - block start;
+ *      static(c) / dynamic(c) (modelled as static(c)):
+ *                 chunk k = p / c belongs to task k mod T; it is that task's
+ *                 (k / T)-th chunk, so p's position is (k / T) * c + p mod c;
+ *      none:      task p (error if n > T), position 0.
+ *    The child's list length is own()'s count for t, in closed form
+ *    (or_own_count); tests pin both against or_own / or_nest_run / brute.py.
+ *    Every level must be bound to loop 0.  Returns the mixed-radix leaf id
+ *    (the same packing as task_gid), or a negative error code.
+ * ======================================================================== */
+int64_t or_own_count(int32_t sched, int64_t chunk, int64_t n, int64_t T, int64_t t) {
+  if (T < 1 || t < 0 || t >= T || n < 0) return OR_E_INVALID;
+  if (sched == OR_STATIC) return n / T + (t < n % T ? 1 : 0);
+  if (sched == OR_STATIC_CHUNK || sched == OR_DYNAMIC) {
+    if (chunk < 1) return OR_E_INVALID;
+    const int64_t full = n / chunk, rest = n % chunk;        /* whole chunks, ragged tail */
+    int64_t cnt = (full / T + (t < full % T ? 1 : 0)) * chunk;  /* whole chunks of task t   */
+    if (rest > 0 && full % T == t) cnt += rest;               /* the tail chunk is number full */
+    return cnt;
+  }
+  if (sched == OR_NONE) {
+    if (n > T) return OR_E_SCHEDULE;
+    return t < n ? 1 : 0;
+  }
+  return OR_E_INVALID;
+}
+
+int64_t or_owner_flat(const or_level* lv, int nlev, int64_t n, int64_t i) {
+  if (nlev < 1 || nlev > 16 || i < 0 || i >= n) return OR_E_INVALID;
+  int64_t p = i, len = n, leaf = 0;
+  for (int a = 0; a < nlev; ++a) {
+    const or_level* L = &lv[a];
+    if (L->loop != 0 || L->T < 1) return OR_E_INVALID;
+    int64_t t = 0, pos = 0;
+    if (L->sched == OR_STATIC) {
+      const int64_t q = len / L->T, r = len % L->T;
+      /* blocks 0..r-1 have q+1 positions, the rest q */
+      if (p < r * (q + 1)) {
+        t = p / (q + 1);
+        pos = p - t * (q + 1);
+      } else {
+        t = r + (p - r * (q + 1)) / q;
+        pos = p - (t * q + r);
+      }
+    } else if (L->sched == OR_STATIC_CHUNK || L->sched == OR_DYNAMIC) {
+      if (L->chunk < 1) return OR_E_INVALID;
+      const int64_t k = p / L->chunk;
+      t = k % L->T;
+      pos = (k / L->T) * L->chunk + p % L->chunk;
+    } else if (L->sched == OR_NONE) {
+      if (len > L->T) return OR_E_SCHEDULE;
+      t = p;
+      pos = 0;
+    } else {
+      return OR_E_INVALID;
+    }
+    len = or_own_count(L->sched, L->chunk, len, L->T, t);
+    if (len < 0) return len;
+    p = pos;
+    leaf = leaf * L->T + t;
+  }
+  return leaf;
+}
+
+/* Fingerprints of the iterations [begin, begin + count) of a flat nest over
+ * n iterations, computed one iteration at a time from or_owner_flat:
+ *   out[0] += sum fp_mix(g0 + i),  out[1] += sum fp_mix2(g0 + i, owner(i))
+ * (mod 2^64), g0 = the global index of iteration 0 (the rank's first).  The
+ * sums are exact in Z/2^64, so disjoint ranges may be fingerprinted
+ * separately and added.  Returns OR_OK or a negative error. */
+int or_fp_flat_range(const or_level* lv, int nlev, int64_t n, int64_t begin, int64_t count, uint64_t g0,
+                     uint64_t* out) {
+  if (begin < 0 || count < 0 || begin + count > n) return OR_E_INVALID;
+  uint64_t f_once = 0, f_owner = 0;
+  for (int64_t i = begin; i < begin + count; ++i) {
+    const int64_t o = or_owner_flat(lv, nlev, n, i);
+    if (o < 0) return (int)o;
+    f_once += or_fp_mix(g0 + (uint64_t)i);
+    f_owner += or_fp_mix2(g0 + (uint64_t)i, (uint64_t)o);
+  }
+  out[0] += f_once;
+  out[1] += f_owner;
+  return OR_OK;
 }
 
 /* The recurrence the affine fold computes, run directly: y <- a_i*y + b_i for

@@ -89,6 +89,13 @@ def lib():
         L.or_fp_mix2.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         L.or_fp_once.restype = ctypes.c_uint64
         L.or_fp_once.argtypes = [ctypes.c_uint64, ctypes.c_int64]
+        L.or_own_count.restype = ctypes.c_int64
+        L.or_own_count.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
+        L.or_owner_flat.restype = ctypes.c_int64
+        L.or_owner_flat.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64]
+        L.or_fp_flat_range.restype = ctypes.c_int
+        L.or_fp_flat_range.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p]
         L.or_fp_owner.restype = ctypes.c_uint64
         L.or_fp_owner.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64]
     return _lib
@@ -271,3 +278,36 @@ def fp_owner(owner: np.ndarray, begin: int) -> int:
 def affine_run(x: np.ndarray, y0: int = 0) -> int:
     x = np.ascontiguousarray(x, dtype=np.int64)
     return int(lib().or_affine_run(_ptr(x), x.size, y0))
+
+
+# --------------------------------------------------------------------------
+# per-iteration owners of flat nests and range fingerprints (full sizes)
+# --------------------------------------------------------------------------
+def _levels_arr(levels):
+    return (_Level * len(levels))(*[_Level(l.sched, l.loop, l.chunk, l.T) for l in levels])
+
+
+def own_count(sched: int, chunk: int, n: int, T: int, t: int) -> int:
+    c = int(lib().or_own_count(sched, chunk, n, T, t))
+    if c < 0:
+        raise OracleError(c, "own_count")
+    return c
+
+
+def owner_flat(levels: list[Level], n: int, i: int) -> int:
+    arr = _levels_arr(levels)
+    o = int(lib().or_owner_flat(ctypes.cast(arr, ctypes.c_void_p), len(levels), n, i))
+    if o < 0:
+        raise OracleError(o, "owner_flat")
+    return o
+
+
+def fp_flat_range(levels: list[Level], n: int, begin: int, count: int, g0: int = 0) -> tuple[int, int]:
+    """(F_once, F_owner) of iterations [begin, begin + count) of a flat nest
+    over n iterations (mod 2^64; disjoint ranges add)."""
+    arr = _levels_arr(levels)
+    out = np.zeros(2, dtype=np.uint64)
+    rc = lib().or_fp_flat_range(ctypes.cast(arr, ctypes.c_void_p), len(levels), n, begin, count, g0, _ptr(out))
+    if rc != 0:
+        raise OracleError(rc, "fp_flat_range")
+    return int(out[0]), int(out[1])
