@@ -89,8 +89,11 @@ typedef struct {
   int64_t max_num;         /* launch limit per parent (oversubscription bound)        */
   uint64_t localmem_bytes; /* memory shared by the siblings (Table 2 localmem)        */
   uint64_t groupmem_bytes; /* memory private to each task (Table 2 groupmem)          */
-  double grainedness;      /* relative task duration; synchronisation cost in SM
-                              cycles of this level's combine/barrier          */
+  double grainedness;      /* relative task duration: an ESTIMATED synchronisation
+                              cost in SM cycles of this level's combine/barrier
+                              (not measured on B200 — B300 latencies for
+                              CTA/warp/lane, order-of-magnitude figures above;
+                              only the inward-shrinking order is meaningful)         */
 } hpar_level_info;
 
 /* A device description.  hpar_device_describe() fills it from the CUDA
@@ -121,9 +124,12 @@ hpar_status hpar_hierarchy_describe(const hpar_device_desc* dev, int32_t nranks,
                                     hpar_level_info out[HPAR_NLEVELS], int32_t* nlevels);
 
 /* §8(a) A0: the level table of `device`, with the GPU level's num = the size
- * of `nccl_comm` (an ncclComm_t borrowed from the caller; NULL = 1 GPU) and
- * the cluster level's num from cudaOccupancyMaxActiveClusters for the
- * default geometry (K=2, W=8). */
+ * of `nccl_comm` (ncclCommCount of an ncclComm_t borrowed from the caller;
+ * NULL = 1 GPU) and the cluster level's num = cudaOccupancyMaxActiveClusters
+ * of the flat streaming kernel in the default geometry (K = 2 CTAs of W = 8
+ * consumer warps + 1 producer warp, 64 KiB ring): the clusters that can run
+ * at once (P:139 num), GPC placement included.  Also the default C of
+ * hpar_nest_create (one wave of co-resident clusters). */
 hpar_status hpar_hierarchy_query(int32_t device, void* nccl_comm, hpar_level_info out[HPAR_NLEVELS],
                                  int32_t* nlevels);
 
@@ -236,6 +242,7 @@ typedef enum { HPAR_OP_SUM = 0, HPAR_OP_MIN = 1, HPAR_OP_MAX = 2, HPAR_OP_HIST25
 typedef enum { HPAR_I32 = 0, HPAR_I64 = 1, HPAR_F32 = 2, HPAR_F64 = 3, HPAR_U8 = 4, HPAR_U64 = 5 } hpar_dtype;
 
 enum { HPAR_VERIFY_COVERAGE = 1, HPAR_VERIFY_PARTIALS = 2, HPAR_VERIFY_FINGERPRINT = 4 };
+enum { HPAR_LOCAL_N0_EMPTY = -1 };  /* hpar_reduce_desc.local_n0: an empty caller-sharded shard */
 
 typedef struct {
   int32_t op;            /* hpar_op                                                        */
@@ -268,9 +275,11 @@ typedef struct {
   uint64_t* fingerprint;    /* verify: uint64[3] += {F_once, F_owner, iterations}         */
   uint64_t global_begin;    /* global index of this rank's first iteration (fingerprints) */
   int64_t local_n0;         /* CSR only: this rank's row count when the caller shards rows
-                               by nonzeros (hpar_shard_range_csr); 0 = the GPU level's
-                               static block of n0.  A rank whose shard is empty skips the
-                               call (keyed results have no node-level collective)         */
+                               by nonzeros (hpar_shard_range_csr); 0 = not caller-sharded
+                               (the GPU level's static block of n0); HPAR_LOCAL_N0_EMPTY
+                               (-1) = this rank's caller-sharded shard has no rows: the
+                               call validates and returns HPAR_OK without a launch (keyed
+                               results have no node-level collective)                     */
 } hpar_reduce_desc;
 
 /* §8(e) C3: nnz-balanced contiguous row shards of a CSR matrix over

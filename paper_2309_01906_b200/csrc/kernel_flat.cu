@@ -219,6 +219,31 @@ cudaError_t launch_flat(const NestArgs& a, int W, cudaStream_t s, const char** n
   return cudaErrorInvalidValue;
 }
 
+// clusters of K CTAs of the flat kernel (W consumer warps + the producer,
+// the 4-stage ring of g_flat_tile fp32) that fit on the device at once
+// (cudaOccupancyMaxActiveClusters: counts SMs, per-SM residency and the GPC
+// placement of clusters).  0 on error.
+int flat_max_active_clusters(int K, int W) {
+  auto kern = flat_tma_kernel<float, double, OP_SUM, false>;
+  const size_t smem = (size_t)kStages * g_flat_tile * 4;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  if (K > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)K);
+  cfg.blockDim = dim3((unsigned)((W + 1) * 32));
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)K;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return 0;
+  return n;
+}
+
 int flat_resident_ctas_per_sm(int W) {
   int n = 0;
   auto kern = flat_tma_kernel<float, double, OP_SUM, false>;

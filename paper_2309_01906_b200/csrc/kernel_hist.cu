@@ -128,6 +128,14 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
 #define HPAR_INC(w, k) inc_shared(region + __byte_perm((w), col, 0x5504u | ((k) << 4)))
     const int nvec = tile / 16;
     const int64_t leaf = (int64_t)a.rank * a.threads_per_gpu + b * W * 32 + threadIdx.x;
+    unsigned long long fpo = 0, fpw = 0, fpn = 0;  // verify: coverage fingerprints
+    auto visit = [&](int64_t it) {  // verify bookkeeping of one iteration (byte) of this lane
+      if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
+      if (a.verify & V_FINGERPRINT) {
+        const uint64_t g = a.global_begin + (uint64_t)it;
+        fpo += fp_mix(g); fpw += fp_mix2(g, (uint64_t)leaf); fpn += 1;
+      }
+    };
     int s = 0;
     uint32_t ph = 0;
     for (int64_t j = 0; j < my_tiles; ++j) {
@@ -155,10 +163,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
         }
         if constexpr (VERIFY) {
           for (int f = warp * 32 + lane; f < nvec; f += W * 32)
-            for (int e = 0; e < 16; ++e) {
-              const int64_t it = base + 16 * f + e;
-              if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
-            }
+            for (int e = 0; e < 16; ++e) visit(base + 16 * f + e);
         }
       } else if (len == tile && !mis) {
 #pragma unroll 2
@@ -174,10 +179,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
             HPAR_INC(w, 3);
           }
           if constexpr (VERIFY) {
-            for (int e = 0; e < 16; ++e) {
-              const int64_t it = base + 16 * f + e;
-              if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
-            }
+            for (int e = 0; e < 16; ++e) visit(base + 16 * f + e);
           }
         }
       } else {
@@ -188,15 +190,20 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
             if (off >= len) break;
             const uint32_t byte = off < in_smem ? st[off] : x[base + off];
             inc_shared(region + col + (byte << 8));
-            if constexpr (VERIFY) {
-              if (a.verify & V_COVERAGE) { a.owner[base + off] = leaf; atomicAdd(&a.count[base + off], 1u); }
-            }
+            if constexpr (VERIFY) visit(base + off);
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == nst) { s = 0; ph ^= 1; }
+    }
+    if constexpr (VERIFY) {
+      if (a.verify & V_FINGERPRINT) {
+        atomicAdd(&a.fp[0], fpo);
+        atomicAdd(&a.fp[1], fpw);
+        atomicAdd(&a.fp[2], fpn);
+      }
     }
    };
     switch ((warp >> 1) % R) {
@@ -352,7 +359,6 @@ static int hist_regions(const NestArgs& a, int W) {
 
 bool hist_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 1 || a.keyed || a.op != OP_HIST || a.in_dtype != DT_U8) { *why = "flat u8 hist"; return false; }
-  if (a.verify & V_FINGERPRINT) { *why = "fingerprints not produced by the hist kernel"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
   LevelView v = device_levels(a);
   if (v.n != 4) { *why = "needs cluster, CTA, warp, lane levels"; return false; }

@@ -41,6 +41,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <algorithm>
+#include <mutex>
 #include <type_traits>
 #include "fused_common.cuh"
 
@@ -307,6 +308,12 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       }
       ++ni;
     };
+    if constexpr (DEEP) {
+      // slots 2 and 3 alias E and off, last written by generic-proxy stores
+      // in phase 1: order those writes before the async-proxy (TMA) writes
+      fence_proxy_async_shared();
+      __syncwarp();
+    }
     int iw = 0;
     for (int d = 0; d < NS && iw < n; ++d, iw += WIN) seg_issue(iw);
     double acc = 0.0;
@@ -782,11 +789,21 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
   ws.tickets = (unsigned int*)p;
   ws.q_cap = maxseg;
   ws.dbg_t = nullptr;
+  // process-wide debug buffer and tensor-map cache: guarded, and the debug
+  // buffer regrows when a call has more warps than the last
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   static unsigned long long* dbg_buf = nullptr;
+  static int64_t dbg_warps = 0;
   const bool times = getenv("HPAR_SEG_TIMES") != nullptr;
   const int64_t nwarps = a.C * a.K * WARPS;
   if (times) {
-    if (!dbg_buf) cudaMalloc(&dbg_buf, nwarps * 6 * 8);
+    if (nwarps > dbg_warps) {
+      cudaFree(dbg_buf);
+      dbg_buf = nullptr;
+      dbg_warps = 0;
+      if (cudaMalloc(&dbg_buf, nwarps * 6 * 8) == cudaSuccess) dbg_warps = nwarps;
+    }
     ws.dbg_t = dbg_buf;
   }
   cudaLaunchConfig_t cfg = {};

@@ -35,8 +35,9 @@ cudaError_t launch_rowwise(const NestArgs& a, int W, cudaStream_t s, const char*
 bool hist_matches(const NestArgs& a, const char** why);
 cudaError_t launch_hist(const NestArgs& a, int W, cudaStream_t s, const char** name);
 int flat_resident_ctas_per_sm(int W);
+int flat_max_active_clusters(int K, int W);
 bool segmented_matches(const NestArgs& a, const char** why);
-cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaStream_t s, const char** name);
+cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t ws_nnz, cudaStream_t s, const char** name);
 size_t segmented_ws_bytes(int64_t nnz);
 void segmented_ws_qrow(int64_t nnz, size_t* off, size_t* len);
 cudaError_t launch_affine_rank_fold(const void* gathered, int G, void* out, cudaStream_t s);
@@ -165,8 +166,12 @@ uint32_t level_props(int level) {
   return 0;
 }
 
-// Grainedness: the SM-cycle cost of one combine/barrier step among
-// the level's siblings (B300_MICROARCH measured constants).
+// Grainedness (units unspecified): an ESTIMATE of the SM-cycle
+// cost of one combine/barrier step among the level's siblings.  Not measured
+// on B200: the CTA / warp / lane figures are the B300 (sm_103a) latencies of
+// barrier.cluster, bar.sync and SHFL from B300_MICROARCH.md, the cluster and
+// GPU figures order-of-magnitude kernel-boundary and small-NCCL-allreduce
+// costs.  Only their order (shrinking inward) is relied upon.
 double level_grain(int level) {
   switch (level) {
     case HPAR_NODE: return 1e6;
@@ -253,7 +258,10 @@ extern "C" hpar_status hpar_hierarchy_query(int32_t device, void* nccl_comm, hpa
   }
   CUDA_TRY(cudaSetDevice(device));
   const int K = 2, W = 8;
-  int64_t C = (int64_t)d.sm_count * hpar::flat_resident_ctas_per_sm(W) / K;
+  // P:139 num = the tasks the level can run at once: the clusters of the
+  // default geometry that are co-resident (occupancy API, GPC placement incl.)
+  const int64_t C = hpar::flat_max_active_clusters(K, W);
+  if (C < 1) return fail(HPAR_E_CUDA, "cudaOccupancyMaxActiveClusters failed for the K=%d, W=%d geometry", K, W);
   return hpar_hierarchy_describe(&d, nranks, K, W, C, out, nlevels);
 }
 
@@ -284,6 +292,7 @@ struct hpar_nest {
   void* gather_buf = nullptr;  // node level of ordered ops: G gathered results
   void* seg_ws = nullptr;  // CSR segmented kernel workspace (grown on demand)
   size_t seg_ws_bytes = 0;
+  int64_t seg_ws_nnz = -1;  // the nnz the workspace layout was built for (its capacity)
   float* halo_buf = nullptr;  // ghost exchange staging (grown on demand)
   size_t halo_bytes = 0;
   // fused node level (HPAR_NEST_NODE_FUSED; node_fused.cuh)
@@ -471,7 +480,9 @@ extern "C" hpar_status hpar_nest_create(const hpar_nest_level* lv, int32_t nleve
       cudaDeviceProp p;
       cudaError_t e = cudaGetDeviceProperties(&p, cfg->device);
       if (e != cudaSuccess) return bail(fail(HPAR_E_CUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e)));
-      C = std::max<int64_t>(1, (int64_t)p.multiProcessorCount * hpar::flat_resident_ctas_per_sm((int)W) / K);
+      // the co-resident clusters of the flat kernel for this (K, W): one wave
+      C = hpar::flat_max_active_clusters((int)K, (int)W);
+      if (C < 1) C = std::max<int64_t>(1, (int64_t)p.multiProcessorCount * hpar::flat_resident_ctas_per_sm((int)W) / K);
     }
   }
   n->G = n->nranks;
@@ -713,10 +724,14 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
 
   int64_t begin = 0, local = 0;
   shard_of(n, d->n0, n->rank, &begin, &local);
-  if (d->local_n0 > 0) {  // caller-sharded CSR rows (hpar_shard_range_csr, §8(e) C3)
+  bool empty_shard = false;
+  if (d->local_n0 > 0 || d->local_n0 == HPAR_LOCAL_N0_EMPTY) {  // caller-sharded CSR rows (§8(e) C3)
     if (!d->offsets || !d->keyed || d->local_n0 > d->n0)
       return fail(HPAR_E_INVALID, "local_n0 is for keyed CSR calls (and <= n0)");
-    local = d->local_n0;
+    local = d->local_n0 > 0 ? d->local_n0 : 0;
+    empty_shard = local == 0;
+  } else if (d->local_n0 < 0) {
+    return fail(HPAR_E_INVALID, "local_n0 %lld: > 0 rows, 0 = unset, or HPAR_LOCAL_N0_EMPTY", (long long)d->local_n0);
   }
   if (local > 0 && !d->in) return fail(HPAR_E_INVALID, "in is NULL");
 
@@ -775,7 +790,7 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   if (node_in_kernel) {
     A.node_dc = n->node_dc_dev;
     A.node_win = n->node_win;
-    A.node_parity = (int32_t)(n->node_calls++ & 1);
+    A.node_parity = (int32_t)(n->node_calls & 1);  // advanced only once the launch succeeded
     A.node_slot = (int32_t)kNodeSlot;
   }
 
@@ -830,6 +845,10 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
     A.out_dtype = (d->in_dtype == HPAR_F32 || d->in_dtype == HPAR_F64) ? HPAR_F64 : HPAR_I64;
   }
 
+  if (empty_shard) {  // nothing to reduce on this rank; keyed results need no node level
+    n->last_kernel = "none (empty shard)";
+    return ok();
+  }
   // ---- kernel choice: fused specialisation if the nest matches its shape ----
   const char* why = nullptr;
   const char* name = "generic";
@@ -846,12 +865,17 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
     e = launch_rowwise(A, (int)n->W, stream, &name);
   } else if (segmented_matches(A, &why)) {
     // CSR: n1 = nonzeros of this rank's shard (local offsets start at 0)
+    // The workspace layout (queue, partials, tickets) is a function of the
+    // nnz it was built for, never of the current call's: a later call with
+    // fewer nonzeros keeps the same offsets, so the self-reset tickets and the
+    // all-ones empty queue slots stay where the kernel looks for them.
     const int64_t nnz = d->n1;
-    const size_t need = segmented_ws_bytes(nnz);
-    if (need > n->seg_ws_bytes) {
+    if (nnz > n->seg_ws_nnz) {
+      const size_t need = segmented_ws_bytes(nnz);
       cudaFree(n->seg_ws);
       n->seg_ws = nullptr;
       n->seg_ws_bytes = 0;
+      n->seg_ws_nnz = -1;
       cudaError_t ae = cudaMalloc(&n->seg_ws, need);
       if (ae != cudaSuccess) return fail(HPAR_E_NOMEM, "segmented workspace (%zu B): %s", need, cudaGetErrorString(ae));
       size_t qoff, qlen;
@@ -859,8 +883,9 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
       CUDA_TRY(cudaMemsetAsync(n->seg_ws, 0, need, stream));
       CUDA_TRY(cudaMemsetAsync((char*)n->seg_ws + qoff, 0xFF, qlen, stream));  // empty queue slots = -1
       n->seg_ws_bytes = need;
+      n->seg_ws_nnz = nnz;
     }
-    e = launch_segmented(A, n->seg_ws, nnz, stream, &name);
+    e = launch_segmented(A, n->seg_ws, n->seg_ws_nnz, stream, &name);
   } else if (teams_matches(A, &why)) {
     e = launch_teams(A, (int)n->W, stream, &name);
   } else if (collapsed) {
@@ -885,6 +910,7 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   }
   if (e != cudaSuccess) return fail(HPAR_E_CUDA, "launch %s: %s", name, cudaGetErrorString(e));
   n->last_kernel = name;
+  if (node_in_kernel) ++n->node_calls;  // every rank advances the slot parity in step
 
   // ---- node level: one allreduce over NVLink (§8(a) A9) ----
   if (node_in_kernel) {

@@ -32,6 +32,7 @@ STATIC, STATIC_CHUNK, DYNAMIC, NONE = 0, 1, 2, 3
 OP_SUM, OP_MIN, OP_MAX, OP_HIST256, OP_AFFINE = 0, 1, 2, 3, 4
 I32, I64, F32, F64, U8, U64 = 0, 1, 2, 3, 4, 5
 VERIFY_COVERAGE, VERIFY_PARTIALS, VERIFY_FINGERPRINT = 1, 2, 4
+LOCAL_N0_EMPTY = -1  # hpar_reduce_desc.local_n0 of an empty caller-sharded shard
 MAX_NEST = 8
 
 
@@ -330,7 +331,7 @@ def dtype_code(t) -> int:
 def make_desc(x, out, *, op: int = OP_SUM, n0: int, n1: int = 0, ld: int = 0, nloops: int = 1,
               keyed: bool = False, offsets=None, max_inner: int = 0, out_dtype: int = -1, verify: int = 0,
               partials=None, owner=None, count=None, fingerprint=None, global_begin: int = 0,
-              local_n0: int = 0) -> ReduceDesc:
+              local_n0: int | None = None) -> ReduceDesc:
     """Build an hpar_reduce_desc from torch tensors (device pointers only)."""
     d = ReduceDesc()
     d.op = op
@@ -350,7 +351,8 @@ def make_desc(x, out, *, op: int = OP_SUM, n0: int, n1: int = 0, ld: int = 0, nl
     d.coverage_count = count.data_ptr() if count is not None else None
     d.fingerprint = fingerprint.data_ptr() if fingerprint is not None else None
     d.global_begin = global_begin
-    d.local_n0 = local_n0
+    # local_n0: None = not caller-sharded; a row count (0 = this rank's shard is empty)
+    d.local_n0 = 0 if local_n0 is None else (local_n0 if local_n0 > 0 else LOCAL_N0_EMPTY)
     return d
 
 

@@ -3,10 +3,13 @@ times (same nests, geometry and kernels):
 
   C2  65536 x 4096 fp32: every row vs the oracle's fp64 row sums
   C3  2^24 rows / 2^28 nonzeros: every row vs the oracle's segment sums
-  C4  2^32 bytes: bins = sum of the cluster partials, sampled cluster
-      partials vs the oracle's histogram of that cluster's bytes, total count
-  C5  2^34 fp32 (64 GiB): sampled cluster partials vs the oracle's fp64 sum of
-      that cluster's elements; total = fold of the cluster partials
+  C4  2^32 bytes: all bins vs the oracle's histogram of the whole input;
+      coverage fingerprints (F_once, F_owner, count) vs the oracle's; cluster
+      partials sum to the bins, sampled ones vs the oracle
+  C5  2^34 fp32 (64 GiB): the total vs the oracle's exact sum; coverage
+      fingerprints vs the oracle's; sampled cluster partials vs the oracle
+The oracle runs range by range in a process pool (tests/fullsize_oracle.py:
+every quantity is exact and additive over disjoint ranges).
 Inputs come from the device generator, which is cross-checked bit for bit
 against inputs/gen.py in test_gpu_parity.py."""
 import ctypes
@@ -80,26 +83,53 @@ def _cluster_tiles(c, C, K, tile, n):
     return [(b, min(b + chunk, n)) for b in range(c * chunk, n, C * chunk)]
 
 
-def test_c4_full_sampled(env, oracle):
+def _flat_levels(C, K, W, tile, V):
+    """the c4/c5 nest [GPU static, cluster static(K tile), CTA static(tile),
+    warp static(32 V), lane static(V)] at G = 1, in the oracle's numbering"""
+    return [(1, 0, 0), (C, 1, K * tile), (K, 1, tile), (W, 1, 32 * V), (32, 1, V)]
+
+
+def test_c4_full(env, oracle):
+    """C4 at 2^32 bytes in bench.py's timed launch (K, W, C) = (2, 8, 74):
+    all 256 bins bit-exact against the oracle's histogram of the whole input;
+    then a verify run of the same geometry: per-iteration coverage by
+    fingerprints (F_once = every byte exactly once, F_owner = each byte's
+    owner is the oracle's leaf for it, count = 2^32), cluster partials summing
+    to the bins, sampled cluster partials against the oracle's bytes."""
+    from tests import fullsize_oracle as F
     torch, H, nests, L = env
     K, W, C = bench_geometry("c4")
     n = 1 << 32
     tile = nests.TILE_U8
     nest = H.Nest(nests.c4_nest(K), device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+    assert nest.info().C == C
     x = torch.empty(n, dtype=torch.uint8, device="cuda")
     L.hpar_inputs_fill_u8(gen.SEED_C4, 0, n, x.data_ptr(), None)
     out = torch.zeros(256, dtype=torch.int64, device="cuda")
-    levels = nest.levels
-    clus = torch.zeros((C, 256), dtype=torch.int64, device="cuda")
-    parts = [None] * len(levels)
-    parts[1] = clus  # level 1 = the cluster level of c4_nest
-    nest.parallel_for_reduce(H.make_desc(x, out, n0=n, op=H.OP_HIST256, verify=H.VERIFY_PARTIALS,
-                                         partials=parts))
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=n, op=H.OP_HIST256))
     torch.cuda.synchronize()
+    assert nest.last_kernel() == "hist256_lanepriv_tma"
     bins = out.cpu().numpy().astype(np.uint64)
+    want = F.histogram(gen.SEED_C4, n)
+    assert np.array_equal(bins, want)
+    # verify run: fingerprints + cluster partials
+    out.zero_()
+    clus = torch.zeros((C, 256), dtype=torch.int64, device="cuda")
+    fp = torch.zeros(3, dtype=torch.int64, device="cuda")
+    parts = [None] * len(nest.levels)
+    parts[1] = clus  # level 1 = the cluster level of c4_nest
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=n, op=H.OP_HIST256, verify=H.VERIFY_PARTIALS | H.VERIFY_FINGERPRINT,
+                                         partials=parts, fingerprint=fp))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "hist256_lanepriv_tma"
+    assert np.array_equal(out.cpu().numpy().astype(np.uint64), want)
+    f = [int(v) for v in fp.cpu().numpy().view(np.uint64)]
+    once, own = F.flat_fingerprints(_flat_levels(C, K, W, tile, 16), n)
+    assert f[2] == n, "iterations executed"
+    assert f[0] == once, "F_once: some byte missed or visited twice"
+    assert f[1] == own, "F_owner: some byte executed by another leaf than the oracle's"
     cl = clus.cpu().numpy().astype(np.uint64)
-    assert int(bins.sum()) == n
-    assert np.array_equal(cl.sum(axis=0), bins)
+    assert np.array_equal(cl.sum(axis=0), want)
     for c in (0, C // 2, C - 1):
         h = np.zeros(256, dtype=np.uint64)
         for b, e in _cluster_tiles(c, C, K, tile, n):
@@ -107,31 +137,52 @@ def test_c4_full_sampled(env, oracle):
         assert np.array_equal(cl[c], h), f"cluster {c}"
 
 
-def test_c5_full_sampled(env, oracle):
+def test_c5_full(env, oracle):
+    """C5 at 2^34 fp32 (64 GiB) in bench.py's timed launch: the total within
+    1e-5 of the oracle's (the exact sum: every input is k 2^-24, so the
+    oracle's Σk over the whole input, range by range, gives it exactly); a
+    verify run of the same geometry: fingerprints (F_once, F_owner, count
+    = 2^34) against the oracle's, sampled cluster partials against the
+    oracle's sums of those clusters' elements, total = fold of the cluster
+    partials."""
+    from tests import fullsize_oracle as F
     torch, H, nests, L = env
     K, W, C = bench_geometry("c5")
     n = 1 << 34
     tile = nests.TILE_F32
     nest = H.Nest(nests.c5_nest(K), device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
-    C = nest.info().C
+    C = nest.info().C  # bench's default: the resident clusters (a launch parameter, checked by F_owner)
     x = torch.empty(n, dtype=torch.float32, device="cuda")
     L.hpar_inputs_fill_f32(gen.SEED_C5, 0, n, x.data_ptr(), None)
     out = torch.zeros(1, dtype=torch.float64, device="cuda")
-    clus = torch.zeros(C, dtype=torch.float64, device="cuda")
-    parts = [None] * len(nest.levels)
-    parts[1] = clus
-    nest.parallel_for_reduce(H.make_desc(x, out, n0=n, verify=H.VERIFY_PARTIALS, partials=parts))
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=n))
     torch.cuda.synchronize()
     assert nest.last_kernel() == "flat_tma"
-    cl = clus.cpu().numpy()
     tot = float(out.item())
-    assert_rel(np.array([tot]), np.array([float(np.sum(cl))]), tol=1e-9)
+    exact = F.exact_numerator_sum(gen.SEED_C5, n) * 2.0 ** -24
+    assert_rel(np.array([tot]), np.array([exact]))
+    # verify run
+    out.zero_()
+    clus = torch.zeros(C, dtype=torch.float64, device="cuda")
+    fp = torch.zeros(3, dtype=torch.int64, device="cuda")
+    parts = [None] * len(nest.levels)
+    parts[1] = clus
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=n, verify=H.VERIFY_PARTIALS | H.VERIFY_FINGERPRINT,
+                                         partials=parts, fingerprint=fp))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "flat_tma"
+    f = [int(v) for v in fp.cpu().numpy().view(np.uint64)]
+    once, own = F.flat_fingerprints(_flat_levels(C, K, W, tile, 4), n)
+    assert f[2] == n, "iterations executed"
+    assert f[0] == once, "F_once: some element missed or visited twice"
+    assert f[1] == own, "F_owner: some element executed by another leaf than the oracle's"
+    cl = clus.cpu().numpy()
+    assert_rel(np.array([float(out.item())]), np.array([float(np.sum(cl))]), tol=1e-9)
+    assert_rel(np.array([float(out.item())]), np.array([exact]))
     for c in (0, C - 1):
         s = 0
         for b, e in _cluster_tiles(c, C, K, tile, n):
             s += oracle.sum_u64(gen.gen_f32_k(gen.SEED_C5, b, e - b))
         assert_rel(np.array([cl[c]]), np.array([s * 2.0 ** -24]))
-    # the total against the exact closed form is too slow on one core
-    # (2^34 generator draws); the total's pieces are all pinned above
     del x
     torch.cuda.empty_cache()

@@ -41,6 +41,9 @@ def _worker(port, q):
         from paper_2309_01906_b200 import nests
         comm = H.torch_nccl_comm()
         res = {}
+        # A0: the GPU level's num through ncclCommCount of the borrowed communicator
+        t = H.hpar_hierarchy_query(0, comm)
+        q_gpu_num = (int(t[H.HPAR_GPU].num), dist.get_world_size())
 
         def run(levels, x, op, n0, reps=3, **kw):
             outs = []
@@ -73,7 +76,7 @@ def _worker(port, q):
         res["generic_affine"] = run([H.Level(1, 3, H.STATIC), H.Level(4, 5, H.STATIC)],
                                     gen.gen_i32(gen.SEED_C1, 0, 70_001).astype(np.int64), H.OP_AFFINE, 70_001,
                                     clusters=2)
-        q.put(("ok", res))
+        q.put(("ok", (res, q_gpu_num)))
         dist.destroy_process_group()
     except Exception as e:  # report, do not hang the parent
         import traceback
@@ -89,6 +92,8 @@ def test_node_level_in_kernel():
     status, res = q.get(timeout=540)
     p.join(60)
     assert status == "ok", res
+    res, (gpu_num, world) = res
+    assert gpu_num == world == 1, "hierarchy query GPU num = ncclCommCount of the communicator"
     from inputs import gen
     from oracle import oracle as O
     n = (1 << 22) + 5
@@ -103,5 +108,13 @@ def test_node_level_in_kernel():
             assert np.array_equal(a, b), (name, a, b)   # same kernel, same tree: bit-identical
         if want.get(name) is not None:
             assert np.array_equal(fused[0].astype(np.int64).ravel()[: np.size(want[name])], np.asarray(want[name]).ravel())
+    # the ordered op against the oracle (not only fused vs host): block
+    # schedules at every level, so the composed map is the oracle's direct
+    # recurrence y <- (2x+1) y + x^2 over the 70,001 elements in order
+    xa = gen.gen_i32(gen.SEED_C1, 0, 70_001).astype(np.int64)
+    for got in res["generic_affine"][0][1]:
+        A, B = (int(v) for v in np.asarray(got).view(np.uint64).ravel()[:2])
+        for y0 in (0, 5, 123456789):
+            assert (A * y0 + B) % (1 << 64) == O.affine_run(xa, y0)
     whole = O.sum_u64(gen.gen_f32_k(gen.SEED_C5, 0, n))
     assert abs(res["flat"][0][1][0][0] - whole * 2.0 ** -24) <= 1e-9 * whole * 2.0 ** -24

@@ -121,7 +121,10 @@ def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, 
 
 
 def compare(oracle, H, levels, res, x, *, n0, n1=0, offsets=None, keyed=False, op=0, C, K, W,
-            dynamic=False, partials=True):
+            dynamic=False, partials=True, unmaterialised=()):
+    """unmaterialised: the nest levels whose partials the kernel documents it
+    does not produce (they must stay at the -7 fill); every other requested
+    level must equal the oracle's."""
     ol = oracle_levels(oracle, levels, 1, C, K, W)
     o = oracle.nest_run(ol, n0=n0, n1=n1, offsets=offsets, x=x, op=op, keyed=keyed,
                         nloops=2 if (n1 or offsets is not None) else 1)
@@ -143,9 +146,10 @@ def compare(oracle, H, levels, res, x, *, n0, n1=0, offsets=None, keyed=False, o
         for a, p in enumerate(res["parts"]):
             if p is None or o.partials[a] is None:
                 continue
+            if a in unmaterialised:
+                assert np.all(p == -7), f"level {a}: documented as not materialised, but written"
+                continue
             if op in (H.OP_HIST256, H.OP_AFFINE):
-                if np.all(p == -7):
-                    continue  # level without materialised bins (lanes)
                 assert np.array_equal(p.view(np.uint64), o.partials[a]), f"level {a} partials"
             elif fp:
                 assert_rel(p, o.partials[a])
@@ -635,3 +639,92 @@ def test_segmented_explicit_zeros(H, torch_mod, oracle, values):
     torch.cuda.synchronize()
     assert nest.last_kernel() == "segmented_csr"
     assert_rel(out.cpu().numpy(), oracle.segsum_f32(v, off))
+
+
+def test_segmented_nest_reuse_shrinking_nnz(H, torch_mod, oracle):
+    """One Nest called with a large CSR (long rows > 4096 nonzeros), then with
+    smaller ones that still hold long rows, then the large one again: the
+    segment workspace keeps the layout of its capacity, so tickets and the
+    empty queue slots stay where the kernel looks."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    rng = np.random.default_rng(4242)
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=6)
+
+    def case(rows, p_long):
+        lens = np.where(rng.random(rows) < p_long, rng.integers(4097, 60000, rows), rng.geometric(0.1, rows))
+        off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        return off, gen.gen_f32(gen.SEED_C3, 0, int(off[-1]))
+
+    cases = [case(4000, 0.02), case(600, 0.05), case(50, 0.2), case(4000, 0.02)]
+    for off, v in cases + cases[::-1]:
+        rows = off.size - 1
+        out = torch.full((rows,), -1.0, dtype=torch.float64, device="cuda")
+        d = H.make_desc(torch.from_numpy(v).cuda(), out, n0=rows, n1=v.size, nloops=2, keyed=True,
+                        offsets=torch.from_numpy(off).cuda(), out_dtype=H.F64)
+        nest.parallel_for_reduce(d)
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "segmented_csr"
+        assert_rel(out.cpu().numpy(), oracle.segsum_f32(v, off))
+
+
+def test_segmented_empty_caller_shard(H, torch_mod):
+    """A caller-sharded CSR rank with no rows (local_n0 = 0 ->
+    HPAR_LOCAL_N0_EMPTY) returns without a launch and writes nothing (ADVICE
+    r01: it used to fall back to the static block of n0 rows)."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    nest = H.Nest(nests.c3_fast_nest(), device=0, rank=1, nranks=2, cluster_dim=2, warps_per_cta=8, clusters=2)
+    off = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = torch.full((1,), -3.0, dtype=torch.float32, device="cuda")
+    x = torch.zeros(4, dtype=torch.float32, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=100, n1=0, nloops=2, keyed=True, offsets=off, local_n0=0))
+    torch.cuda.synchronize()
+    assert float(out.item()) == -3.0
+    assert nest.last_kernel().startswith("none")
+
+
+def test_hierarchy_query_cluster_num_is_occupancy(H, torch_mod):
+    """P:139 num(c): the cluster level's num equals cudaOccupancyMaxActiveClusters
+    for the flat kernel's launch shape (288 threads, a 64 KiB ring, clusters of
+    2), cross-checked through the driver API on a stand-in kernel of the same
+    footprint compiled here with NVRTC (cuda-python; nothing from libhpar)."""
+    from cuda.bindings import driver as cu
+    from cuda.bindings import nvrtc
+    torch = torch_mod
+    torch.cuda.init()
+    t = H.hpar_hierarchy_query(0)
+    src = b'extern "C" __global__ void standin(float* o) { extern __shared__ float s[]; ' \
+          b'if (o) o[threadIdx.x] = s[threadIdx.x]; }'
+    err, prog = nvrtc.nvrtcCreateProgram(src, b"standin.cu", 0, [], [])
+    assert err == nvrtc.nvrtcResult.NVRTC_SUCCESS
+    err, = nvrtc.nvrtcCompileProgram(prog, 1, [b"--gpu-architecture=sm_100a"])
+    assert err == nvrtc.nvrtcResult.NVRTC_SUCCESS
+    err, size = nvrtc.nvrtcGetCUBINSize(prog)
+    cubin = b" " * size
+    err, = nvrtc.nvrtcGetCUBIN(prog, cubin)
+    assert err == nvrtc.nvrtcResult.NVRTC_SUCCESS
+    err, = cu.cuInit(0)
+    err, ctx = cu.cuDevicePrimaryCtxRetain(0)
+    err, = cu.cuCtxSetCurrent(ctx)
+    err, mod = cu.cuModuleLoadData(cubin)
+    assert err == cu.CUresult.CUDA_SUCCESS, err
+    err, fn = cu.cuModuleGetFunction(mod, b"standin")
+    smem = 4 * 4096 * 4 + 256  # the ring + the kernel's static barriers / climb slots (< 1 KiB)
+    err, = cu.cuFuncSetAttribute(fn, cu.CUfunction_attribute.CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem)
+    cfg = cu.CUlaunchConfig()
+    cfg.gridDimX, cfg.gridDimY, cfg.gridDimZ = 2, 1, 1
+    cfg.blockDimX, cfg.blockDimY, cfg.blockDimZ = 9 * 32, 1, 1
+    cfg.sharedMemBytes = smem
+    attr = cu.CUlaunchAttribute()
+    attr.id = cu.CUlaunchAttributeID.CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION
+    attr.value.clusterDim.x, attr.value.clusterDim.y, attr.value.clusterDim.z = 2, 1, 1
+    cfg.attrs = [attr]
+    cfg.numAttrs = 1
+    err, nclus = cu.cuOccupancyMaxActiveClusters(fn, cfg)
+    assert err == cu.CUresult.CUDA_SUCCESS, err
+    assert t[H.HPAR_CLUSTER].num == nclus
+    assert t[H.HPAR_CTA].num == 2 and t[H.HPAR_WARP].num == 8
+    # the default geometry of a nest is the same single wave
+    from paper_2309_01906_b200 import nests
+    assert H.Nest(nests.c5_nest(2), device=0, cluster_dim=2, warps_per_cta=8).info().C == nclus
