@@ -2,17 +2,20 @@
 """bench.py — throughput of the hpar hot path on B200 (BASELINE.json metric:
 "elements/s and HBM GB/s (% of peak) for nested reductions at 1/2/4/8 B200").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c5|c4|c1|c3] [--impl hpar|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c2|c4|c1|c3|c6] [--impl hpar|reference]
 
 A step is one hpar_parallel_for_reduce over one batch of the config's
 synthetic workload (seeded generator, inputs/gen.py recipe), inputs resident
-in HBM.  Default workload: config 2 (BASELINE.json configs[1]), the 4-level
-row-wise nest over a 65536 x 4096 fp32 matrix per GPU (weak scaling: each
-rank reduces its own 65536-row shard; rows are independent, no collective).
-Config 5 (2^34 fp32 flat sum over the GPUs, one NCCL allreduce) is
-strong-scaled.  Under torchrun one process per GPU; rank 0 prints ONE JSON
-line.  `--impl reference` times the CPU oracle (the reference arm for this
-tier) on a bounded sample of the same workload.
+in HBM.  Default workload: config 5 (BASELINE.json configs[4], the largest
+single-GPU configuration): the 5-level flat nest GPU -> cluster -> CTA ->
+warp -> lane summing 2^34 fp32 (64 GiB), strong-scaled over the GPUs with
+one NCCL allreduce at the node level.  Config 2 (configs[1], the 4-level
+row-wise nest over ONE 65536 x 4096 fp32 matrix) is strong-scaled too: its
+rows are sharded over the GPUs.  `--gpus N` without a
+launcher spawns N ranks itself (torch.distributed.run, one process per GPU,
+127.0.0.1 rendezvous); under torchrun WORLD_SIZE must equal N.  Rank 0 prints
+ONE JSON line.  `--impl reference` times the CPU oracle (the reference arm
+for this tier) on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -101,11 +104,10 @@ class ClockSampler:
 # --------------------------------------------------------------- configs --
 def config_spec(name: str, nranks: int):
     from inputs import gen
-    if name == "c2":
+    if name == "c2":  # one 65536 x 4096 matrix, rows sharded over the GPUs
         rows, cols = 65536, 4096
-        return dict(workload="c2_rowwise_4level_65536x4096_f32", kind="rowwise", rows_per_rank=rows, cols=cols,
-                    n0=rows * nranks, scaling="weak", seed=gen.SEED_C2, dtype="f32",
-                    elems_per_rank=rows * cols, bytes_per_rank=rows * cols * 4 + rows * 4)
+        return dict(workload="c2_rowwise_4level_65536x4096_f32", kind="rowwise", cols=cols,
+                    n0=rows, scaling="strong", seed=gen.SEED_C2, dtype="f32", elems_total=rows * cols)
     if name == "c5":
         n = 1 << 34
         return dict(workload="c5_flat_5level_2^34_f32", kind="flat", n0=n, scaling="strong", seed=gen.SEED_C5,
@@ -562,12 +564,54 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(n: int, argv: list[str]) -> int:
+    """Run this script as n ranks (one process per GPU) under
+    torch.distributed.run on this node, 127.0.0.1 rendezvous; returns the
+    launcher's exit code.  The native library is built once, before the
+    ranks start."""
+    if "--check-launch" not in argv:
+        from paper_2309_01906_b200 import build as pbuild
+        pbuild.build()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
+
+
+def check_launch(args):
+    """--check-launch: the launcher's plumbing without a GPU — every rank
+    joins a gloo process group, the ranks' ids are summed, rank 0 prints the
+    world size it saw (tests/test_bench_contract.py)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([rank], dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"check_launch": True, "n_gpus": world, "rank_sum": int(t.item())}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
+    ap.add_argument("--check-launch", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--impl", default="hpar", choices=["hpar", "reference"])
     ap.add_argument("--node", default="nccl", choices=["nccl", "fused"],
                     help="node level of total reductions at N>1: host ncclAllReduce, or in-kernel (NEXT f1)")
@@ -580,7 +624,17 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" in os.environ:
+        if int(os.environ["WORLD_SIZE"]) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE="
+                             f"{os.environ['WORLD_SIZE']} ranks")
+    elif args.gpus > 1:
+        sys.exit(launch_ranks(args.gpus, sys.argv[1:]))
+    if args.check_launch:
+        check_launch(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_hpar(args)

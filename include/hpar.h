@@ -302,16 +302,39 @@ hpar_status hpar_shard_range_csr(const int64_t* offsets, int64_t rows, int32_t n
  * levels lack), HPAR_E_CUDA, HPAR_E_NCCL.  Empty loops yield the identity. */
 hpar_status hpar_parallel_for_reduce(hpar_nest_t nest, const hpar_reduce_desc* desc, void* stream);
 
-/* §8(a) A10: a barrier among the sibling tasks of hardware level `level`
- * (S:344-352).  HPAR_GPU: a cross-rank rendezvous on the stream (NCCL).
- * HPAR_CLUSTER: HPAR_E_CAPABILITY (clusters have no barrier; P:178 read as
- * "does not support").  HPAR_CTA / HPAR_WARP / HPAR_LANE: launches the
- * level's barrier in the §3.7 fallback pattern: every task
- * writes f(its id) to its slot, the level barrier runs, every task reads all
- * sibling slots and folds them; if `probe_mismatches` (device uint64) is
- * non-NULL the number of tasks whose fold differs from the expected value is
- * added to it (0 = barrier visibility holds).  HPAR_NODE: no-op. */
-hpar_status hpar_barrier(hpar_nest_t nest, int32_t level, uint64_t* probe_mismatches, void* stream);
+/* §8(a) A10: a host-level barrier among the sibling tasks of hardware level
+ * `level`, enqueued on `stream`.
+ *   HPAR_GPU:     a cross-rank rendezvous on the stream (a 1-int NCCL
+ *                 allreduce over the nest's communicator; no-op with 1 rank).
+ *   HPAR_CLUSTER: HPAR_E_CAPABILITY — clusters have no barrier (P:178 read
+ *                 as "does not support"; S:348 diagnose, never UB).
+ *   HPAR_CTA / HPAR_WARP / HPAR_LANE / HPAR_NODE: HPAR_OK, nothing enqueued.
+ *                 Between two calls every task of these levels has finished
+ *                 and its writes are visible at the kernel boundary, which
+ *                 stream order already provides; INSIDE a
+ *                 call these levels synchronise with __syncwarp / bar.sync /
+ *                 barrier.cluster (probed by hpar_barrier_probe).
+ * Errors: HPAR_E_INVALID (NULL nest, bad level, describe-only nest),
+ * HPAR_E_CAPABILITY, HPAR_E_NCCL. */
+hpar_status hpar_barrier(hpar_nest_t nest, int32_t level, void* stream);
+
+/* Verify call for the in-kernel level barriers (§8(c) #5; the §3.7 fallback
+ * pattern P:308-323, generalised by S:360 "every lane gets 36").  Launches
+ * the nest's C clusters x K CTAs x W warps; for `rounds` rounds every task of
+ * `level` (HPAR_CTA: each CTA; HPAR_WARP: each warp; HPAR_LANE: each lane)
+ * writes fp_mix((round << 40) ^ id) to its slot — id = the task's linear id
+ * on the GPU (CTA: blockIdx; warp: blockIdx * W + warp; lane: blockIdx *
+ * 32 W + thread) — the level's barrier runs, and the task adds the sum of
+ * its siblings' slots (mod 2^64) to a running fold.  folds[task] (device
+ * uint64, C*K / C*K*W / C*K*W*32 entries, caller-owned) receives the fold
+ * over all rounds; the caller compares it with the group sums computed
+ * independently (the oracle's fp_mix).  flags HPAR_PROBE_NO_BARRIER: the
+ * negative control — the barrier is omitted and sibling k delays its write
+ * by (k+1) * delay_ns, so readers fold stale slots.  Errors:
+ * HPAR_E_CAPABILITY (HPAR_CLUSTER), HPAR_E_INVALID, HPAR_E_CUDA. */
+enum { HPAR_PROBE_NO_BARRIER = 1 };
+hpar_status hpar_barrier_probe(hpar_nest_t nest, int32_t level, int32_t rounds, uint32_t flags, uint32_t delay_ns,
+                               uint64_t* folds, void* stream);
 
 /* ---- property-based level selection (§3.2-3.3) --------------
  * A construct `parallel sync(demand) reserve(sync(reserve))` asks for levels

@@ -25,8 +25,8 @@
 
 namespace hpar {
 cudaError_t launch_generic(const NestArgs& a, int threads, cudaStream_t s);
-cudaError_t launch_probe(int level, int64_t C, int K, int W, int rounds, unsigned long long* mismatches,
-                         cudaStream_t s);
+cudaError_t launch_probe(int level, int64_t C, int K, int W, int rounds, int no_barrier, uint32_t delay_ns,
+                         unsigned long long* folds, cudaStream_t s);
 // fused specialisations (kernel_flat.cu, kernel_rowwise.cu, kernel_hist.cu)
 bool flat_matches(const NestArgs& a, const char** why);
 cudaError_t launch_flat(const NestArgs& a, int W, cudaStream_t s, const char** name);
@@ -949,26 +949,40 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
 }
 
 // ----------------------------------------------------------- barriers ----
-extern "C" hpar_status hpar_barrier(hpar_nest_t n, int32_t level, uint64_t* mismatches, void* stream_) {
+extern "C" hpar_status hpar_barrier(hpar_nest_t n, int32_t level, void* stream_) {
   if (!n) return fail(HPAR_E_INVALID, "hpar_barrier: NULL nest");
   if (level < HPAR_NODE || level > HPAR_LANE) return fail(HPAR_E_INVALID, "bad level %d", level);
   if (!(level_props(level) & HPAR_P_BARRIER) && level != HPAR_NODE)
     return fail(HPAR_E_CAPABILITY, "barrier on the %s level, which has no `barrier` property (S:348; P:178)",
                 kLevelNames[level]);
   if (n->device < 0) return fail(HPAR_E_INVALID, "describe-only nest cannot execute");
-  cudaStream_t stream = (cudaStream_t)stream_;
-  if (level == HPAR_NODE) return ok();
+  // node: one process per GPU, the node is the job; CTA / warp / lane: every
+  // task of a call has finished (and its writes are visible) at the kernel
+  // boundary, which stream order already puts between consecutive calls
+  if (level != HPAR_GPU) return ok();
+  if (n->nranks == 1 || !n->comm) return ok();
   CUDA_TRY(cudaSetDevice(n->device));
-  if (level == HPAR_GPU) {
-    if (n->nranks == 1 || !n->comm) return ok();
-    hpar_status s = need_nccl();
-    if (s) return s;
-    ncclResult_t r = g_nccl.allReduce(n->barrier_word, n->barrier_word, 1, ncclInt32, ncclSum, (ncclComm_t)n->comm,
-                                      stream);
-    if (r != ncclSuccess) return nccl_fail(r, (ncclComm_t)n->comm, "ncclAllReduce (barrier)");
-    return ok();
-  }
-  cudaError_t e = launch_probe(level, n->C, (int)n->K, (int)n->W, 8, (unsigned long long*)mismatches, stream);
+  hpar_status s = need_nccl();
+  if (s) return s;
+  ncclResult_t r = g_nccl.allReduce(n->barrier_word, n->barrier_word, 1, ncclInt32, ncclSum, (ncclComm_t)n->comm,
+                                    (cudaStream_t)stream_);
+  if (r != ncclSuccess) return nccl_fail(r, (ncclComm_t)n->comm, "ncclAllReduce (barrier)");
+  return ok();
+}
+
+extern "C" hpar_status hpar_barrier_probe(hpar_nest_t n, int32_t level, int32_t rounds, uint32_t flags,
+                                          uint32_t delay_ns, uint64_t* folds, void* stream_) {
+  if (!n) return fail(HPAR_E_INVALID, "hpar_barrier_probe: NULL nest");
+  if (level != HPAR_CTA && level != HPAR_WARP && level != HPAR_LANE)
+    return fail(level == HPAR_CLUSTER ? HPAR_E_CAPABILITY : HPAR_E_INVALID,
+                "barrier probe: in-kernel levels only (cta, warp, lane); %s",
+                level == HPAR_CLUSTER ? "clusters have no barrier (P:178)" : "bad level");
+  if (rounds < 1 || !folds) return fail(HPAR_E_INVALID, "barrier probe: rounds >= 1 and folds[] required");
+  if (flags & ~(uint32_t)HPAR_PROBE_NO_BARRIER) return fail(HPAR_E_INVALID, "barrier probe: unknown flags");
+  if (n->device < 0) return fail(HPAR_E_INVALID, "describe-only nest cannot execute");
+  CUDA_TRY(cudaSetDevice(n->device));
+  cudaError_t e = launch_probe(level, n->C, (int)n->K, (int)n->W, rounds, (flags & HPAR_PROBE_NO_BARRIER) ? 1 : 0,
+                               delay_ns, (unsigned long long*)folds, (cudaStream_t)stream_);
   if (e != cudaSuccess) return fail(HPAR_E_CUDA, "barrier probe: %s", cudaGetErrorString(e));
   return ok();
 }

@@ -32,6 +32,7 @@ STATIC, STATIC_CHUNK, DYNAMIC, NONE = 0, 1, 2, 3
 OP_SUM, OP_MIN, OP_MAX, OP_HIST256, OP_AFFINE = 0, 1, 2, 3, 4
 I32, I64, F32, F64, U8, U64 = 0, 1, 2, 3, 4, 5
 VERIFY_COVERAGE, VERIFY_PARTIALS, VERIFY_FINGERPRINT = 1, 2, 4
+PROBE_NO_BARRIER = 1  # hpar_barrier_probe flag: the negative control
 LOCAL_N0_EMPTY = -1  # hpar_reduce_desc.local_n0 of an empty caller-sharded shard
 MAX_NEST = 8
 
@@ -152,7 +153,9 @@ def lib() -> ctypes.CDLL:
             "hpar_shard_range": [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
                                  ctypes.POINTER(ctypes.c_int64)],
             "hpar_parallel_for_reduce": [ctypes.c_void_p, ctypes.POINTER(ReduceDesc), ctypes.c_void_p],
-            "hpar_barrier": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p],
+            "hpar_barrier": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p],
+            "hpar_barrier_probe": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint32,
+                                   ctypes.c_void_p, ctypes.c_void_p],
             "hpar_nest_resolve": [ctypes.POINTER(SyncConstruct), ctypes.c_int32, ctypes.POINTER(LevelInfo),
                                   ctypes.POINTER(NestLevel)],
             "hpar_level_alias": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
@@ -303,16 +306,26 @@ class Nest:
     def parallel_for_reduce(self, desc: ReduceDesc, stream: int = 0) -> None:
         _check(lib().hpar_parallel_for_reduce(self.handle, ctypes.byref(desc), stream))
 
-    def barrier(self, level: int, mismatches_ptr: int = 0, stream: int = 0) -> None:
-        _check(lib().hpar_barrier(self.handle, level, mismatches_ptr or None, stream))
+    def barrier(self, level: int, stream: int = 0) -> None:
+        _check(lib().hpar_barrier(self.handle, level, stream))
+
+    def barrier_probe(self, level: int, folds_ptr: int, rounds: int = 8, no_barrier: bool = False,
+                      delay_ns: int = 0, stream: int = 0) -> None:
+        _check(lib().hpar_barrier_probe(self.handle, level, rounds, PROBE_NO_BARRIER if no_barrier else 0,
+                                        delay_ns, folds_ptr, stream))
 
 
 def hpar_parallel_for_reduce(nest: Nest, desc: ReduceDesc, stream: int = 0) -> None:
     nest.parallel_for_reduce(desc, stream)
 
 
-def hpar_barrier(nest: Nest, level: int, mismatches_ptr: int = 0, stream: int = 0) -> None:
-    nest.barrier(level, mismatches_ptr, stream)
+def hpar_barrier(nest: Nest, level: int, stream: int = 0) -> None:
+    nest.barrier(level, stream)
+
+
+def hpar_barrier_probe(nest: Nest, level: int, folds_ptr: int, rounds: int = 8, no_barrier: bool = False,
+                       delay_ns: int = 0, stream: int = 0) -> None:
+    nest.barrier_probe(level, folds_ptr, rounds, no_barrier, delay_ns, stream)
 
 
 # ---- torch convenience ------------------------------------------------------

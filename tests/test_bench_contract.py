@@ -23,3 +23,32 @@ def test_reference_arm_line(config):
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["unit"] == line["unit"]
     assert "workload" in line["config"]
+
+
+def _env_without_launcher():
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    return env
+
+
+def test_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` with no launcher spawns 2 ranks itself
+    (torch.distributed.run, 127.0.0.1); they meet in a process group (gloo on
+    the CPU here, NCCL on the GPU box) and rank 0 reports the world size."""
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--check-launch"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=300, env=_env_without_launcher())
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    assert lines[0]["n_gpus"] == 2 and lines[0]["rank_sum"] == 1
+
+
+def test_gpus_flag_must_match_launcher():
+    """Under a launcher, WORLD_SIZE != --gpus fails loudly (it never times one
+    GPU while claiming N)."""
+    env = _env_without_launcher()
+    env.update(WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--check-launch"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=120, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr

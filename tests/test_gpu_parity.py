@@ -445,20 +445,64 @@ def test_segmented_csr_kernel(H, torch_mod, oracle, case):
                 assert (ws_ == ws_[0]).all(), "a block's short rows span several warps"
 
 
-def test_barrier_probes(H, torch_mod):
-    """§8(a) A10: lane / warp / CTA barriers give rendezvous + visibility
-    (0 mismatches); the cluster level has no barrier."""
-    from paper_2309_01906_b200 import nests
+def _probe_expect(oracle, level, C, K, W, rounds):
+    """The oracle's fold for every task of the probe (hpar_barrier_probe):
+    sum over rounds of the sum over the task's sibling group of
+    fp_mix((round << 40) ^ sibling id), mod 2^64.  Groups: the 32 lanes of a
+    warp, the W warps of a CTA, the K CTAs of a cluster."""
+    M = (1 << 64) - 1
+    group = {"lane": 32, "warp": W, "cta": K}[level]
+    ntask = {"lane": C * K * W * 32, "warp": C * K * W, "cta": C * K}[level]
+    out = np.zeros(ntask, dtype=np.uint64)
+    for g0 in range(0, ntask, group):
+        f = 0
+        for r in range(rounds):
+            f += sum(oracle.fp_mix((r << 40) ^ (g0 + j)) for j in range(group))
+        out[g0:g0 + group] = f & M
+    return out
+
+
+def test_barrier_probes(H, torch_mod, oracle):
+    """§8(a) A10 / §8(c) #5: with the lane / warp / CTA barriers of the hot
+    path (__syncwarp, bar.sync, barrier.cluster) every task's folds over its
+    siblings' slots equal the oracle's group folds; host-level hpar_barrier
+    on those levels is the kernel boundary (OK, nothing enqueued); the
+    cluster level has no barrier."""
     torch = torch_mod
-    nest = H.Nest(nests.c5_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=37)
-    mm = torch.zeros(1, dtype=torch.int64, device="cuda")
+    C, K, W, R = 37, 2, 8, 8
+    nest = H.Nest([H.Level(H.HPAR_GPU, H.HPAR_LANE)], device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+    for name, lvl in (("lane", H.HPAR_LANE), ("warp", H.HPAR_WARP), ("cta", H.HPAR_CTA)):
+        want = _probe_expect(oracle, name, C, K, W, R)
+        folds = torch.zeros(want.size, dtype=torch.int64, device="cuda")
+        nest.barrier_probe(lvl, folds.data_ptr(), rounds=R)
+        torch.cuda.synchronize()
+        assert np.array_equal(folds.cpu().numpy().view(np.uint64), want), f"{name}: folds differ from the oracle's"
     for lvl in (H.HPAR_LANE, H.HPAR_WARP, H.HPAR_CTA, H.HPAR_NODE, H.HPAR_GPU):
-        nest.barrier(lvl, mm.data_ptr())
+        nest.barrier(lvl)
     torch.cuda.synchronize()
-    assert int(mm.item()) == 0
-    with pytest.raises(H.HparError) as e:
-        nest.barrier(H.HPAR_CLUSTER, mm.data_ptr())
-    assert e.value.code == H.HPAR_E_CAPABILITY
+    for call in (lambda: nest.barrier(H.HPAR_CLUSTER),
+                 lambda: nest.barrier_probe(H.HPAR_CLUSTER, folds.data_ptr())):
+        with pytest.raises(H.HparError) as e:
+            call()
+        assert e.value.code == H.HPAR_E_CAPABILITY
+
+
+@pytest.mark.parametrize("level", ["warp", "cta"])
+def test_barrier_probe_negative_control(H, torch_mod, oracle, level):
+    """The probe pins something: with the level barrier removed and sibling k
+    writing (k+1) x 2 us late, readers fold stale slots and the folds differ
+    from the oracle's.  (The lane level's control is left to racecheck:
+    lanes reconverge after the divergent delay, profiles/r02_sanitizer.md.)"""
+    torch = torch_mod
+    C, K, W, R = 37, 2, 8, 4
+    nest = H.Nest([H.Level(H.HPAR_GPU, H.HPAR_LANE)], device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+    lvl = {"warp": H.HPAR_WARP, "cta": H.HPAR_CTA}[level]
+    want = _probe_expect(oracle, level, C, K, W, R)
+    folds = torch.zeros(want.size, dtype=torch.int64, device="cuda")
+    nest.barrier_probe(lvl, folds.data_ptr(), rounds=R, no_barrier=True, delay_ns=2000)
+    torch.cuda.synchronize()
+    bad = int((folds.cpu().numpy().view(np.uint64) != want).sum())
+    assert bad > 0, "a probe without its barrier still folded every slot correctly"
 
 
 def test_hierarchy_query_matches_device(H, torch_mod):
