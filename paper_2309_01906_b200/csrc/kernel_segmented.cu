@@ -91,7 +91,7 @@ struct SegWS {
   unsigned long long* q_tail;        // long-row segments appended
   unsigned long long* q_head;        // long-row segments claimed
   unsigned long long* blocks_done;   // row blocks finished
-  unsigned long long* warps_done;    // warps exited (last one resets)
+  unsigned long long* warps_done;    // CTAs exited (the last one resets)
   SegEntry* q;                       // the segment queue
   double* partials;                  // per segment partial sums (by queue index)
   unsigned int* tickets;             // per long row (at its first segment): segments done
@@ -119,8 +119,10 @@ template <typename RT, int LPL, int D>
 struct alignas(1024) WarpSmem {  // 1 KiB: a swizzled TMA box needs 1 KiB-aligned slots
   static constexpr int WIN = 32 * LPL;
   float ring[D][WIN];            // window ring (TMA destinations)
-  double E[32 * (LPL / 2 + 1) + 2];  // window exclusive prefix at even positions q, at
-                                     // q / 2 + q / LPL (one pad per lane: conflict-free)
+  double E[32 * (LPL / 2 + 1) + 2];  // exact path: window exclusive prefix at even positions
+                                     // q, at q / 2 + q / LPL (one pad per lane: conflict-free);
+                                     // fp32 path: the window's segmented sums S[WIN] (swizzled
+                                     // 16-byte chunks) + float2 (carry-in, first head) per lane
   int32_t off[RB + 4];           // the block's RB+1 offsets relative to base
   RT res[RB];                    // the block's row results, flushed coalesced
   unsigned int lmask[RB / 32];   // long rows of the block (bit per row): never flushed here
@@ -128,6 +130,7 @@ struct alignas(1024) WarpSmem {  // 1 KiB: a swizzled TMA box needs 1 KiB-aligne
   int32_t slot_wr[D];            // window position (relative to base) held by each slot
   uint64_t bar[D];               // ring slot "full" barriers
   uint64_t bar2[2];              // the two extra slots of the deep segment ring (D == 2)
+  uint32_t hb[WIN / 32];         // SEGF32: row heads of the current window (bit per position)
 };
 static_assert(RB == 256, "the flush gives each lane 8 consecutive rows");
 static_assert(sizeof(WarpSmem<float, 16, 3>) % 16 == 0 && sizeof(WarpSmem<double, 8, 4>) % 16 == 0, "TMA alignment");
@@ -167,8 +170,8 @@ __device__ __forceinline__ float max_nan_abs(float m, float v) {  // max(m, |v|)
 // the 128-byte swizzle (16-byte chunk c of box row r stored at c ^ (r & 7)),
 // so the lanes' 64-byte runs load without bank conflicts; the array's last
 // partial 32-float row is read directly (limT below).
-template <bool VERIFY, bool OUT_F32, int LPL, int D, bool SWZ = false>
-__global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg, int long_min, int cb,
+template <bool VERIFY, bool OUT_F32, int LPL, int D, bool SWZ = false, bool SEGF32 = false, int MINB = 3>
+__global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg, int long_min, int cb,
                                                                const __grid_constant__ CUtensorMap tmx) {
   using RT = typename std::conditional<OUT_F32, float, double>::type;
   constexpr int WIN = 32 * LPL;
@@ -245,6 +248,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     }
   };
   unsigned long long my_blocks = 0;  // added to blocks_done once, when this warp leaves phase 1
+  bool published = false;            // this lane appended long-row segments to the queue
   unsigned iseq = 0, cseq = 0;       // ring: windows issued / consumed by this warp
   unsigned phases = 0;               // parity bit per ring slot
   const int64_t nnz4 = nnz_all & ~(int64_t)3;
@@ -264,7 +268,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
   auto do_segment = [&](unsigned long long q, auto deep_c) {
     constexpr bool DEEP = decltype(deep_c)::value && D == 2;
     constexpr int NS = DEEP ? 4 : D;
-    auto slot_ptr = [&](int s) -> float* {
+    auto slot_ptr = [&](int s) -> float* {  // DEEP: ring 0, 1, then E, then off + res (2064 contiguous bytes)
       if constexpr (DEEP) return s == 0 ? &sm.ring[0][0] : s == 1 ? &sm.ring[1][0] : s == 2 ? (float*)&sm.E[0] : (float*)&sm.off[0];
       else return &sm.ring[s][0];
     };
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
       ++ni;
     };
     if constexpr (DEEP) {
-      // slots 2 and 3 alias E and off, last written by generic-proxy stores
+      // the extra slots alias E / off, last written by generic-proxy stores
       // in phase 1: order those writes before the async-proxy (TMA) writes
       fence_proxy_async_shared();
       __syncwarp();
@@ -424,6 +428,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
           const int len = e_ - s_;
           const int ns = (int)((len + SEG - 1) / SEG);
           const unsigned long long q = atomicAdd(ws.q_tail, (unsigned long long)ns);
+          published = true;
           for (int j = 0; j < ns; ++j) {
             SegEntry& en = ws.q[q + j];
             en.b = base + s_ + (int64_t)j * SEG;
@@ -527,6 +532,99 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
           if (q >= lim4 && q < p1) v[k] = x[base + q];
         }
       }
+      if constexpr (SEGF32) {
+        // ---- pass A: row heads.  Every row starting inside the window marks
+        // its first position (empty rows and the block end mark harmlessly:
+        // a head only restarts a running sum).
+        if (lane < WIN / 32) sm.hb[lane] = 0u;
+        __syncwarp();
+        for (int r = rcur;; r += 32) {
+          const int i = r + lane;
+          const int s_ = sm.off[i < nr ? i : nr];
+          const bool in = i <= nr && s_ < wend;
+          if (in && s_ >= wr) atomicOr(&sm.hb[(s_ - wr) >> 5], 1u << ((s_ - wr) & 31));
+          if (__ballot_sync(0xffffffffu, in) != 0xffffffffu) break;
+        }
+        __syncwarp();
+        static_assert(!SEGF32 || (LPL == 16 && SWZ), "fp32 segmented windows: 16 positions per lane, swizzled boxes");
+        const unsigned hbits = (sm.hb[lane >> 1] >> ((lane & 1) * 16)) & 0xFFFFu;
+        // ---- lane-local segmented sums (fp32, restart at every head)
+        float S[LPL];
+        float run = 0.f;
+#pragma unroll
+        for (int k = 0; k < LPL; ++k) {
+          run = ((hbits >> k) & 1u) ? v[k] : run + v[k];
+          S[k] = run;
+        }
+        // ---- warp segmented scan of the lanes' open sums: lane l adds the
+        // sum of lanes (start_l, l-1] where start_l is the last lane <= l
+        // holding a head (Hillis-Steele, add at step o iff o <= lim)
+        const unsigned Hm = __ballot_sync(0xffffffffu, hbits != 0u);
+        const unsigned upto = Hm & (0xffffffffu >> (31 - lane));  // heads in lanes [0, l]
+        const int lim = upto ? lane - (31 - __clz(upto)) : lane;
+        float y = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float t = __shfl_up_sync(0xffffffffu, y, o);
+          if (o <= lim) y += t;
+        }
+        float cin = __shfl_up_sync(0xffffffffu, y, 1);  // the open sum entering this lane
+        if (lane == 0) cin = 0.f;
+        const int fh = hbits ? __ffs(hbits) - 1 : LPL;  // positions before it continue cin
+        // ---- publish S (conflict-free: 16-byte chunk j of lane l stored at
+        // j ^ ((l >> 1) & 3)).  Not in place of the values: the ring slot is
+        // a TMA destination, and ordering generic writes before its refill
+        // (fence.proxy.async per window) measured 3% slower.
+        float* sS = (float*)&sm.E[0];
+        float2* sCF = (float2*)(sS + WIN);
+#pragma unroll
+        for (int j = 0; j < LPL / 4; ++j)
+          *(float4*)&sS[LPL * lane + ((j ^ ((lane >> 1) & 3)) << 2)] = make_float4(S[4 * j], S[4 * j + 1], S[4 * j + 2], S[4 * j + 3]);
+        sCF[lane] = make_float2(cin, __int_as_float(fh));
+        __syncwarp();
+        // ---- pass B: one lane per row overlapping the window; a row's part
+        // of the window is the segmented sum at its last position here
+        int r = rcur;
+        for (;;) {
+          const int i = r + lane;
+          const int s_ = sm.off[i < nr ? i : nr];
+          const int e_ = sm.off[i + 1 < nr ? i + 1 : nr];
+          const bool valid = i < nr && s_ < wend;
+          const int sc = min(max(s_ - wr, 0), WIN);
+          const int ec = min(max(e_ - wr, sc), WIN);
+          const int q = ec > sc ? ec - 1 : 0;
+          const int L = q / LPL, k = q % LPL;
+          const float2 cf = sCF[L];
+          float part = sS[LPL * L + (((k >> 2) ^ ((L >> 1) & 3)) << 2) + (k & 3)];
+          if (k < __float_as_int(cf.y)) part += cf.x;
+          double val = ec > sc ? (double)part : 0.0;
+          if (s_ < wr) val += carry;  // the row open from the previous window
+          const bool complete = valid && e_ <= wend;
+          if (complete) sm.res[i] = (RT)val;  // a long row's slot is never flushed
+          if constexpr (VERIFY) {
+            if (valid && !((sm.lmask[i >> 5] >> (i & 31)) & 1u))
+              for (int qq = sc; qq < ec; ++qq) cover_by(base + wr + qq, leaf0 + qq / LPL);
+          }
+          const unsigned vm = __ballot_sync(0xffffffffu, valid);
+          const unsigned cm = __ballot_sync(0xffffffffu, complete);
+          const int cnt = __popc(vm);
+          if (cnt == 0) break;
+          if (!((cm >> (cnt - 1)) & 1u)) {  // the last overlapping row continues
+            carry = __shfl_sync(0xffffffffu, val, cnt - 1);
+            rcur = r + cnt - 1;
+            break;
+          }
+          r += cnt;
+          rcur = r;
+          carry = 0.0;
+          if (cnt < 32) break;
+        }
+        __syncwarp();  // S and ring slot s are free again
+        if (iw < p1) {
+          issue(iw);
+          iw = skip(iw + WIN);
+        }
+      } else {
       // exactness guard: binade span of the window's nonzero magnitudes
       float amax = 0.f;
 #if HPAR_SEG_FMIN
@@ -636,6 +734,7 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
         issue(iw);
         iw = skip(iw + WIN);
       }
+      }  // exact fp64-prefix windows
     }
     // flush: lane l writes rows 8l..8l+7 (long rows excluded)
     {
@@ -671,8 +770,15 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
     }
   }
 
-  if (lane == 0)  // release: this warp's queue entries are visible before its blocks count
-    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ws.blocks_done), "l"(my_blocks) : "memory");
+  // release: this warp's q_tail appends are visible before its blocks count
+  // (readers rely on q_tail being final once blocks_done == nblocks); a warp
+  // that appended nothing has nothing to order and counts relaxed
+  if (__any_sync(0xffffffffu, published)) {
+    if (lane == 0)
+      asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ws.blocks_done), "l"(my_blocks) : "memory");
+  } else if (lane == 0) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(ws.blocks_done), "l"(my_blocks) : "memory");
+  }
 
   if (ws.dbg_t && lane == 0) ws.dbg_t[6 * gwarp + 1] = gtimer();
   // ------------------------------- phase 2: the remaining long-row segments ----
@@ -720,11 +826,15 @@ __global__ void __launch_bounds__(WARPS * 32) segmented_kernel(const __grid_cons
 
   if (ws.dbg_t && lane == 0) ws.dbg_t[6 * gwarp + 2] = gtimer();
   if (ws.dbg_t && lane == 0) { ws.dbg_t[6 * gwarp + 3] = dbg_nseg; ws.dbg_t[6 * gwarp + 4] = dbg_tseg; ws.dbg_t[6 * gwarp + 5] = dbg_tdone; }
-  // --------------------------------------------- exit: last warp resets ----
-  if (lane == 0) {
-    unsigned long long w;  // acq_rel: the last warp sees every warp's counter updates before it resets them
+  // --------------------------------------------- exit: last CTA resets ----
+  // one arrival per CTA: the barrier orders the CTA's warps' counter updates
+  // before thread 0's acq_rel (release is cumulative), and the last CTA sees
+  // every CTA's updates before it resets them
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long w;
     asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(w) : "l"(ws.warps_done) : "memory");
-    if ((int64_t)w == (int64_t)gridDim.x * WARPS - 1) {
+    if ((int64_t)w == (int64_t)gridDim.x - 1) {
       *ws.block_ticket = 0ull;
       *ws.q_tail = 0ull;
       *ws.q_head = 0ull;
@@ -872,9 +982,18 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
   const int lpl = device_levels(a).l[1]->chunk;
   static int dknob = -1;
   if (dknob < 0) dknob = getenv("HPAR_SEG_D") ? atoi(getenv("HPAR_SEG_D")) : 0;
+  static int f32seg = -1;  // (knob) 1 = fp32 segmented windows (same time, fewer instructions)
+  if (f32seg < 0) f32seg = getenv("HPAR_SEG_F32") ? atoi(getenv("HPAR_SEG_F32")) : 0;
   auto launch_v = [&](auto lpl_c, auto d_c) -> cudaError_t {
     constexpr int L = decltype(lpl_c)::value, DD = decltype(d_c)::value;
     if constexpr (L == 16 && DD == 2) {
+      if (tmx_ok && f32seg) {  // fp32 segmented windows (knob)
+        if (a.verify)
+          return f32 ? pick(segmented_kernel<true, true, L, DD, true, true>, sizeof(WarpSmem<float, L, DD>))
+                     : pick(segmented_kernel<true, false, L, DD, true, true>, sizeof(WarpSmem<double, L, DD>));
+        return f32 ? pick(segmented_kernel<false, true, L, DD, true, true>, sizeof(WarpSmem<float, L, DD>))
+                   : pick(segmented_kernel<false, false, L, DD, true, true>, sizeof(WarpSmem<double, L, DD>));
+      }
       if (tmx_ok) {
         if (a.verify)
           return f32 ? pick(segmented_kernel<true, true, L, DD, true>, sizeof(WarpSmem<float, L, DD>))
