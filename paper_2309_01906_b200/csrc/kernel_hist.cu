@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <algorithm>
 #include <type_traits>
 #include "fused_common.cuh"
 
@@ -55,6 +56,151 @@ __device__ __forceinline__ int tab_word(int bin, int warp, int lane) { return bi
 
 __device__ __forceinline__ void inc_shared(uint32_t addr) {
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
+
+// Verify only, shared lane-table regions (R < pairs): the lane and warp
+// levels are folded inside the shared counters, so their partials are built
+// here instead — every byte a lane counts is also added to its lane's and its
+// warp's partial bins in global memory (u64 atomics; exact, slow, verify
+// runs only).  Layout as the tables' export: [CTA*W*32 + warp*32 + lane][256]
+// and [CTA*W + warp][256].
+template <bool VERIFY>
+struct InnerDirect {
+  unsigned long long* lanep = nullptr;
+  unsigned long long* warpp = nullptr;
+  __device__ __forceinline__ InnerDirect(const NestArgs& a, int W, int R) {
+    if constexpr (VERIFY) {
+      if (!(a.verify & V_PARTIALS) || R == (W + 1) / 2) return;
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int lv = 0; lv < a.nlev; ++lv) {
+        if (!a.partials[lv]) continue;
+        if (a.lv[lv].slast == S_LANE_IN)
+          lanep = (unsigned long long*)a.partials[lv] + ((int64_t)blockIdx.x * W * 32 + warp * 32 + lane) * 256;
+        if (a.lv[lv].slast == S_WARP) warpp = (unsigned long long*)a.partials[lv] + ((int64_t)blockIdx.x * W + warp) * 256;
+      }
+      // the bins start at zero (each lane clears its own row and an eighth of
+      // its warp's; the warp's lanes meet before any count is added)
+      for (int k = 0; k < 256; ++k)
+        if (lanep) lanep[k] = 0ull;
+      for (int k = lane; k < 256; k += 32)
+        if (warpp) warpp[k] = 0ull;
+      __syncwarp();
+    }
+  }
+  __device__ __forceinline__ void add(uint32_t byte) const {
+    if constexpr (VERIFY) {
+      if (lanep) atomicAdd(lanep + byte, 1ull);
+      if (warpp) atomicAdd(warpp + byte, 1ull);
+    }
+  }
+};
+
+// lane -> warp -> CTA -> cluster -> GPU (-> node) of the per-lane tables,
+// shared by the TMA-ring and register-streaming kernels.  `counts`: the R
+// lane-table regions; `wbins`: W x 256 u32 scratch; the caller has synced the
+// CTA after the stream.  Lane / warp partials come from the tables only when
+// every warp pair has its own region (R == pairs); with shared regions the
+// verify stream adds them to the partial arrays directly (see inner_direct).
+template <bool VERIFY>
+__device__ __forceinline__ void hist_climb(const NestArgs& a, int W, int R, const uint32_t* counts,
+                                           uint32_t (*wbins)[256], uint32_t* cbins, int& s_flag) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = a.K;
+  const uint32_t crank = cluster_ctarank();
+  const int64_t cl = blockIdx.x / K;
+  const bool tab_inner = R == (W + 1) / 2;  // lane / warp levels materialised in the tables
+  // lane -> warp: warp w sums the 32 lane columns of its table; lane l owns
+  // bins l, l+32, ...; rotated column order keeps the reads conflict-free.
+  // With shared regions the first 2R warps read the (region, column) tables
+  // and the others contribute zero bins.
+  if (warp < W && warp >= 2 * R) {
+    for (int bin = lane; bin < 256; bin += 32) wbins[warp][bin] = 0;
+  } else if (warp < W) {
+    const uint32_t* tab = counts + (size_t)(warp >> 1) * (kRegion / 4);
+    for (int bin = lane; bin < 256; bin += 32) {
+      uint32_t sacc = 0;
+      for (int k = 0; k < 32; ++k) {
+        const int l = (k + lane) & 31;
+        const uint32_t v = tab[tab_word(bin, warp, l)];
+        sacc += v;
+        if (VERIFY && (a.verify & V_PARTIALS) && tab_inner) {
+          for (int lv = 0; lv < a.nlev; ++lv)
+            if (a.lv[lv].slast == S_LANE_IN && a.partials[lv])
+              ((unsigned long long*)a.partials[lv])[((int64_t)blockIdx.x * W * 32 + warp * 32 + l) * 256 + bin] = v;
+        }
+      }
+      wbins[warp][bin] = sacc;
+      if (VERIFY && (a.verify & V_PARTIALS) && tab_inner) {
+        for (int lv = 0; lv < a.nlev; ++lv)
+          if (a.lv[lv].slast == S_WARP && a.partials[lv])
+            ((unsigned long long*)a.partials[lv])[((int64_t)blockIdx.x * W + warp) * 256 + bin] = sacc;
+      }
+    }
+  }
+  __syncthreads();
+  // warp -> CTA (ascending warp)
+  unsigned long long* parts = (unsigned long long*)a.cluster_partials;
+  for (int bin = threadIdx.x; bin < 256; bin += blockDim.x) {
+    uint32_t sacc = 0;
+    for (int w = 0; w < W; ++w) sacc += wbins[w][bin];
+    cbins[bin] = sacc;
+    if (VERIFY && (a.verify & V_PARTIALS)) {
+      for (int l = 0; l < a.nlev; ++l)
+        if (a.lv[l].slast == S_CTA && a.partials[l])
+          ((unsigned long long*)a.partials[l])[(int64_t)blockIdx.x * 256 + bin] = sacc;
+    }
+  }
+  cluster_sync_all();
+  // CTA -> cluster: reduce-scatter over DSMEM, CTA k owns a bin range
+  {
+    const int lo = (int)(256 * crank / K), hi = (int)(256 * (crank + 1) / K);
+    for (int bin = lo + threadIdx.x; bin < hi; bin += blockDim.x) {
+      unsigned long long sacc = 0;
+      for (int k = 0; k < K; ++k) {
+        uint32_t v;
+        asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(mapa(smem_addr(&cbins[bin]), (uint32_t)k)));
+        sacc += v;
+      }
+      parts[cl * 256 + bin] = sacc;
+      if (VERIFY && (a.verify & V_PARTIALS)) {
+        for (int l = 0; l < a.nlev; ++l)
+          if (a.lv[l].slast == S_CLUSTER && a.partials[l]) ((unsigned long long*)a.partials[l])[cl * 256 + bin] = sacc;
+      }
+    }
+  }
+  __threadfence();
+  cluster_sync_all();  // the whole cluster partial is written (and siblings done reading my bins)
+  // cluster -> GPU: single pass; the leader CTA takes the ticket
+  if (crank == 0) {
+    if (threadIdx.x == 0) {
+      const unsigned t = atomicAdd(a.grid_ticket, 1u);
+      s_flag = (t == (unsigned)(a.C - 1));
+      if (s_flag) __threadfence();
+    }
+    __syncthreads();
+    if (s_flag) {
+      constexpr int NB = 4;  // bins per thread (blockDim.x >= 64)
+      unsigned long long tot[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int bin = threadIdx.x + j * blockDim.x;
+        tot[j] = 0;
+        if (bin >= 256) continue;
+        for (int64_t c = 0; c < a.C; ++c) tot[j] += ((volatile unsigned long long*)parts)[c * 256 + bin];
+        if (VERIFY && (a.verify & V_PARTIALS)) {
+          for (int l = 0; l < a.nlev; ++l)
+            if (a.lv[l].slast == S_GPU && a.partials[l]) ((unsigned long long*)a.partials[l])[bin] = tot[j];
+        }
+      }
+      if (a.node_dc) node_fold_bins<NB>(a, tot);  // the node level in-kernel (f1)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int bin = threadIdx.x + j * blockDim.x;
+        if (bin < 256) ((unsigned long long*)a.out)[bin] = tot[j];
+      }
+      if (threadIdx.x == 0) *a.grid_ticket = 0u;
+    }
+  }
 }
 
 // VPL: 16-byte vectors per lane per tile (tile == 512*W*VPL), 0 = generic
@@ -129,12 +275,14 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
     const int nvec = tile / 16;
     const int64_t leaf = (int64_t)a.rank * a.threads_per_gpu + b * W * 32 + threadIdx.x;
     unsigned long long fpo = 0, fpw = 0, fpn = 0;  // verify: coverage fingerprints
-    auto visit = [&](int64_t it) {  // verify bookkeeping of one iteration (byte) of this lane
+    InnerDirect<VERIFY> inner(a, W, R);
+    auto visit = [&](int64_t it, uint32_t byte) {  // verify bookkeeping of one iteration (byte) of this lane
       if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
       if (a.verify & V_FINGERPRINT) {
         const uint64_t g = a.global_begin + (uint64_t)it;
         fpo += fp_mix(g); fpw += fp_mix2(g, (uint64_t)leaf); fpn += 1;
       }
+      inner.add(byte);
     };
     int s = 0;
     uint32_t ph = 0;
@@ -163,7 +311,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
         }
         if constexpr (VERIFY) {
           for (int f = warp * 32 + lane; f < nvec; f += W * 32)
-            for (int e = 0; e < 16; ++e) visit(base + 16 * f + e);
+            for (int e = 0; e < 16; ++e) visit(base + 16 * f + e, st[16 * f + e]);
         }
       } else if (len == tile && !mis) {
 #pragma unroll 2
@@ -179,7 +327,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
             HPAR_INC(w, 3);
           }
           if constexpr (VERIFY) {
-            for (int e = 0; e < 16; ++e) visit(base + 16 * f + e);
+            for (int e = 0; e < 16; ++e) visit(base + 16 * f + e, st[16 * f + e]);
           }
         }
       } else {
@@ -190,7 +338,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
             if (off >= len) break;
             const uint32_t byte = off < in_smem ? st[off] : x[base + off];
             inc_shared(region + col + (byte << 8));
-            if constexpr (VERIFY) visit(base + off);
+            if constexpr (VERIFY) visit(base + off, byte);
           }
         }
       }
@@ -215,98 +363,7 @@ __global__ void __launch_bounds__(1024, 1) hist_kernel(const __grid_constant__ N
   __syncwarp();
   __syncthreads();
 #undef HPAR_INC
-  // lane -> warp: warp w sums the 32 lane columns of its table; lane l owns
-  // bins l, l+32, ...; rotated column order keeps the reads conflict-free.
-  // With shared regions the first 2R warps read the (region, column) tables
-  // and the others contribute zero bins.
-  if (warp < W && warp >= 2 * R) {
-    for (int bin = lane; bin < 256; bin += 32) wbins[warp][bin] = 0;
-  } else if (warp < W) {
-    const uint32_t* tab = counts + (size_t)(warp >> 1) * (kRegion / 4);
-    for (int bin = lane; bin < 256; bin += 32) {
-      uint32_t sacc = 0;
-      for (int k = 0; k < 32; ++k) {
-        const int l = (k + lane) & 31;
-        const uint32_t v = tab[tab_word(bin, warp, l)];
-        sacc += v;
-        if (VERIFY && (a.verify & V_PARTIALS)) {
-          for (int lv = 0; lv < a.nlev; ++lv)
-            if (a.lv[lv].slast == S_LANE_IN && a.partials[lv])
-              ((unsigned long long*)a.partials[lv])[((int64_t)blockIdx.x * W * 32 + warp * 32 + l) * 256 + bin] = v;
-        }
-      }
-      wbins[warp][bin] = sacc;
-      if (VERIFY && (a.verify & V_PARTIALS)) {
-        for (int lv = 0; lv < a.nlev; ++lv)
-          if (a.lv[lv].slast == S_WARP && a.partials[lv])
-            ((unsigned long long*)a.partials[lv])[((int64_t)blockIdx.x * W + warp) * 256 + bin] = sacc;
-      }
-    }
-  }
-  __syncthreads();
-  // warp -> CTA (ascending warp)
-  unsigned long long* parts = (unsigned long long*)a.cluster_partials;
-  for (int bin = threadIdx.x; bin < 256; bin += blockDim.x) {
-    uint32_t sacc = 0;
-    for (int w = 0; w < W; ++w) sacc += wbins[w][bin];
-    cbins[bin] = sacc;
-    if (VERIFY && (a.verify & V_PARTIALS)) {
-      for (int l = 0; l < a.nlev; ++l)
-        if (a.lv[l].slast == S_CTA && a.partials[l])
-          ((unsigned long long*)a.partials[l])[(int64_t)blockIdx.x * 256 + bin] = sacc;
-    }
-  }
-  cluster_sync_all();
-  // CTA -> cluster: reduce-scatter over DSMEM, CTA k owns a bin range
-  {
-    const int lo = (int)(256 * crank / K), hi = (int)(256 * (crank + 1) / K);
-    for (int bin = lo + threadIdx.x; bin < hi; bin += blockDim.x) {
-      unsigned long long sacc = 0;
-      for (int k = 0; k < K; ++k) {
-        uint32_t v;
-        asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(mapa(smem_addr(&cbins[bin]), (uint32_t)k)));
-        sacc += v;
-      }
-      parts[cl * 256 + bin] = sacc;
-      if (VERIFY && (a.verify & V_PARTIALS)) {
-        for (int l = 0; l < a.nlev; ++l)
-          if (a.lv[l].slast == S_CLUSTER && a.partials[l]) ((unsigned long long*)a.partials[l])[cl * 256 + bin] = sacc;
-      }
-    }
-  }
-  __threadfence();
-  cluster_sync_all();  // the whole cluster partial is written (and siblings done reading my bins)
-  // cluster -> GPU: single pass; the leader CTA takes the ticket
-  if (crank == 0) {
-    if (threadIdx.x == 0) {
-      const unsigned t = atomicAdd(a.grid_ticket, 1u);
-      s_flag = (t == (unsigned)(a.C - 1));
-      if (s_flag) __threadfence();
-    }
-    __syncthreads();
-    if (s_flag) {
-      constexpr int NB = 4;  // bins per thread (blockDim.x >= 64)
-      unsigned long long tot[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        const int bin = threadIdx.x + j * blockDim.x;
-        tot[j] = 0;
-        if (bin >= 256) continue;
-        for (int64_t c = 0; c < a.C; ++c) tot[j] += ((volatile unsigned long long*)parts)[c * 256 + bin];
-        if (VERIFY && (a.verify & V_PARTIALS)) {
-          for (int l = 0; l < a.nlev; ++l)
-            if (a.lv[l].slast == S_GPU && a.partials[l]) ((unsigned long long*)a.partials[l])[bin] = tot[j];
-        }
-      }
-      if (a.node_dc) node_fold_bins<NB>(a, tot);  // the node level in-kernel (f1)
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        const int bin = threadIdx.x + j * blockDim.x;
-        if (bin < 256) ((unsigned long long*)a.out)[bin] = tot[j];
-      }
-      if (threadIdx.x == 0) *a.grid_ticket = 0u;
-    }
-  }
+  hist_climb<VERIFY>(a, W, R, counts, wbins, cbins, s_flag);
 }
 
 template <bool V, int VPL>
@@ -351,7 +408,7 @@ static int hist_regions(const NestArgs& a, int W) {
   const int pairs = (W + 1) / 2;
   static int knob = -2;
   if (knob == -2) knob = getenv("HPAR_C4_REGIONS") ? atoi(getenv("HPAR_C4_REGIONS")) : -1;
-  if (inner_partials(a)) return pairs;
+  if (inner_partials(a) && W <= kMaxPrivW) return pairs;  // the tables hold the lane / warp levels
   int r = knob > 0 ? knob : (W <= kMaxPrivW ? pairs : 2);
   if (r > 3) r = 3;
   return r < pairs ? r : pairs;
@@ -373,8 +430,8 @@ bool hist_matches(const NestArgs& a, const char** why) {
   if (k->sched != SCHED_STATIC_CHUNK || tile % (512 * W) != 0 || tile > 32768) { *why = "CTA static(tile)"; return false; }
   if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster static(K*tile)"; return false; }
   const int R = hist_regions(a, (int)W);
-  if (W > kMaxW || (inner_partials(a) && W > kMaxPrivW) || ring_stages(R, (int)tile + 16) < 2) {
-    *why = "W <= 16 (W <= 6 with lane / warp partials: a 64 KiB lane-table region per warp pair)";
+  if (W > kMaxW || ring_stages(R, (int)tile + 16) < 2) {
+    *why = "W <= 16 consumer warps";
     return false;
   }
   return true;

@@ -108,7 +108,7 @@ def test_c4_full(env, oracle):
     out = torch.zeros(256, dtype=torch.int64, device="cuda")
     nest.parallel_for_reduce(H.make_desc(x, out, n0=n, op=H.OP_HIST256))
     torch.cuda.synchronize()
-    assert nest.last_kernel() == "hist256_lanepriv_tma"
+    assert nest.last_kernel().startswith("hist256_lanepriv")
     bins = out.cpu().numpy().astype(np.uint64)
     want = F.histogram(gen.SEED_C4, n)
     assert np.array_equal(bins, want)
@@ -121,7 +121,7 @@ def test_c4_full(env, oracle):
     nest.parallel_for_reduce(H.make_desc(x, out, n0=n, op=H.OP_HIST256, verify=H.VERIFY_PARTIALS | H.VERIFY_FINGERPRINT,
                                          partials=parts, fingerprint=fp))
     torch.cuda.synchronize()
-    assert nest.last_kernel() == "hist256_lanepriv_tma"
+    assert nest.last_kernel().startswith("hist256_lanepriv")
     assert np.array_equal(out.cpu().numpy().astype(np.uint64), want)
     f = [int(v) for v in fp.cpu().numpy().view(np.uint64)]
     once, own = F.flat_fingerprints(_flat_levels(C, K, W, tile, 16), n)

@@ -171,7 +171,7 @@ def test_node_level_across_gpus(oracle):
                 assert abs(g[0] - exact5) <= 1e-5 * exact5, (r, name)
         for name in ("c4", "c4_fused"):
             kern, got = res[name]
-            assert kern == "hist256_lanepriv_tma"
+            assert kern.startswith("hist256_lanepriv")
             for g in got:
                 assert np.array_equal(g.astype(np.uint64), bins4), (r, name)
         kern, got = res["c1"]

@@ -329,7 +329,7 @@ def test_hist_fused_kernel(H, torch_mod, oracle, n):
     for x in (gen.gen_u8(gen.SEED_C4, 0, n), gen.gen_u8_zipf(gen.SEED_C4, 0, n), np.zeros(n, np.uint8)):
         res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, coverage=n <= 200000,
                        partials=n <= 200000)
-        assert res["kernel"] == "hist256_lanepriv_tma"
+        assert res["kernel"].startswith("hist256_lanepriv")
         assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
         if n <= 200000:
             compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
@@ -348,7 +348,7 @@ def test_hist_misaligned_input(H, torch_mod, oracle, mis):
     for n in (1, 17, 16384 * 2 * 5 + 7, 200000):
         for x in (gen.gen_u8(gen.SEED_C4, 0, n), gen.gen_u8_zipf(gen.SEED_C4, 0, n)):
             res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, misalign=mis)
-            assert res["kernel"] == "hist256_lanepriv_tma"
+            assert res["kernel"].startswith("hist256_lanepriv")
             assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
             compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
 
@@ -356,21 +356,24 @@ def test_hist_misaligned_input(H, torch_mod, oracle, mis):
 @pytest.mark.parametrize("W,tile", [(8, 16384), (16, 8192), (12, 12288)])
 def test_hist_shared_regions(H, torch_mod, oracle, W, tile):
     """W > 6 consumer warps: warp pairs share one lane-table region (the
-    atomics keep it exact; the warp level is folded into the shared counters).
-    Totals, coverage (every byte once, owner = static closed form) and the
-    CTA / cluster / GPU partials vs the oracle; uniform, skewed, all-zero."""
+    atomics keep it exact; the warp level is folded into the shared counters
+    in timed runs).  Totals, coverage (every byte once, owner = static closed
+    form) and the partials of EVERY level vs the oracle — the lane and warp
+    bins of verify runs come from direct per-byte atomics — on uniform,
+    skewed and all-zero bytes (reading #23)."""
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     levels = nests.c4_nest(K=2, tile=tile)
     C, K = 3, 2
     for n in (0, 5, tile * 2 * 7 + 9, 1 << 20):
         for x in (gen.gen_u8(gen.SEED_C4, 0, n), gen.gen_u8_zipf(gen.SEED_C4, 0, n), np.zeros(n, np.uint8)):
-            res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, coverage=n <= 300000,
-                           partials=False)
-            assert res["kernel"] == "hist256_lanepriv_tma"
+            small = n <= 300000
+            res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, coverage=small,
+                           partials=small)
+            assert res["kernel"].startswith("hist256_lanepriv")
             assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
-            if n <= 300000:
-                assert (res["count"] == 1).all()
+            if small:  # every level incl. lane / warp bins (built directly in verify runs), owner map
+                compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
     # outer-level partials (cluster, CTA) with shared regions
     n = tile * 2 * 5 + 3
     x = gen.gen_u8(gen.SEED_C4, 1, n)
