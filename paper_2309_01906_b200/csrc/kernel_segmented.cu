@@ -57,7 +57,8 @@ namespace {
 constexpr int RB = 256;            // rows per block claim
 constexpr int64_t LONG = 4096;     // a row with more nonzeros is split (default; HPAR_SEG_LONG)
 constexpr int64_t SPLIT_MIN = 256;  // smallest split threshold the queue is sized for
-constexpr int64_t SEG = HPAR_SEG_LEN;  // nonzeros per long-row segment (16384: -1.5% vs 8192, 32768 +0.5%, 65536 +6%)
+constexpr int64_t SEG = HPAR_SEG_LEN;  // nonzeros per long-row segment at full size (16384: -1.5% vs 8192, 32768 +0.5%, 65536 +6%)
+constexpr int64_t SEG_MIN = 4096;      // the shortest segment the host may pick (small shards; the queue is sized for it)
 constexpr int WARPS = 8;           // warps per CTA (all workers)
 // kernel variants: LPL = nonzeros per lane per window (the nest's lane
 // static(LPL), 8 or 16), WIN = 32 * LPL per window, D = TMA ring depth
@@ -172,7 +173,7 @@ __device__ __forceinline__ float max_nan_abs(float m, float v) {  // max(m, |v|)
 // partial 32-float row is read directly (limT below).
 template <bool VERIFY, bool OUT_F32, int LPL, int D, bool SWZ = false, bool SEGF32 = false, int MINB = 3>
 __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __grid_constant__ NestArgs a, SegWS ws, int dbg, int long_min, int cb,
-                                                               const __grid_constant__ CUtensorMap tmx) {
+                                                               int seg, const __grid_constant__ CUtensorMap tmx) {
   using RT = typename std::conditional<OUT_F32, float, double>::type;
   constexpr int WIN = 32 * LPL;
   static_assert(!SWZ || LPL == 16, "swizzled windows: 16 rows of 32 floats");
@@ -426,13 +427,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
         lg = e_ - s_ > long_min;
         if (lg) {
           const int len = e_ - s_;
-          const int ns = (int)((len + SEG - 1) / SEG);
+          const int ns = (len + seg - 1) / seg;
           const unsigned long long q = atomicAdd(ws.q_tail, (unsigned long long)ns);
           published = true;
           for (int j = 0; j < ns; ++j) {
             SegEntry& en = ws.q[q + j];
-            en.b = base + s_ + (int64_t)j * SEG;
-            en.len = (len - j * SEG < SEG) ? len - j * SEG : (int)SEG;
+            en.b = base + s_ + (int64_t)j * seg;
+            en.len = (len - j * seg < seg) ? len - j * seg : seg;
             en.k = j;
             en.ns = ns;
           }
@@ -849,7 +850,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
 
 // workspace layout inside the caller-provided buffer
 // upper bound on long-row segments: sum of ceil(len/SEG) over rows longer than LONG
-static int64_t max_segments(int64_t nnz) { return nnz / SEG + nnz / SPLIT_MIN + 64; }
+static int64_t max_segments(int64_t nnz) { return nnz / SEG_MIN + nnz / SPLIT_MIN + 64; }
 
 size_t segmented_ws_bytes(int64_t nnz) {
   return 64 * 8 + (size_t)max_segments(nnz) * (sizeof(SegEntry) + 8 + 4) + 4096;
@@ -976,7 +977,18 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
     static int cbk = -1;
     if (cbk < 0) cbk = getenv("HPAR_SEG_CB") ? atoi(getenv("HPAR_SEG_CB")) : CB;
     if (cbk < 1) cbk = 1;
-    return cudaLaunchKernelEx(&cfg, kern, a, ws, dbg, lmin, cbk, tmx);
+    // segment length: SEG at full size (2^28 nonzeros), halved per halving of
+    // the shard down to SEG_MIN (scripts/sweep_seglen.sh: 16384 / 8192 / 4096
+    // best at 1 / 2 / 4-8 GPUs' shards; HPAR_SEG_LEN_RT overrides)
+    static int segk = -1;
+    if (segk < 0) segk = getenv("HPAR_SEG_LEN_RT") ? atoi(getenv("HPAR_SEG_LEN_RT")) : 0;
+    int seg = (int)SEG;
+    if (segk >= (int)SEG_MIN) {
+      seg = segk;
+    } else {
+      for (int64_t n = a.n1; seg > (int)SEG_MIN && n <= (1ll << 27); n *= 2) seg /= 2;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, a, ws, dbg, lmin, cbk, seg, tmx);
   };
   // variant: LPL from the nest's lane chunk; ring depth D (HPAR_SEG_D knob)
   const int lpl = device_levels(a).l[1]->chunk;
