@@ -396,7 +396,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
   };
   unsigned long long u = claim();
   load_offs(u);
+  // cross-block prefetch (SWZ path): once a block has no window left to
+  // issue, the next block's first window goes into the free ring slot, so
+  // the pipeline does not drain at every block boundary
+  unsigned pre_next = 0;  // windows already issued for the next block (0 / 1)
   while ((int64_t)u < nblocks) {
+    const unsigned pre_here = pre_next;
+    pre_next = 0;
     const unsigned long long u1 = claim();
     const int64_t r0 = (int64_t)u * RB;
     const int nr = (int)((R - r0 < RB) ? (R - r0) : RB);
@@ -497,14 +503,35 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
       }
       ++iseq;
     };
-    int iw = (dbg & 2) ? p1 : skip(0);
-    for (int d = 0; d < D && iw < p1; ++d) {
+    // the next block's first window, into a free slot (its rows are not known
+    // yet, so it is window 0 even if that lies inside a long row: then it is
+    // consumed as a partial window of that row, whose result is never flushed)
+    const int64_t base_next = __shfl_sync(0xffffffffu, offr[0], 0) & ~(int64_t)31;
+    const bool can_pre = SWZ && (dbg & 64) == 0 && (int64_t)u1 < nblocks;
+    auto issue_next = [&]() {
+      if constexpr (SWZ) {
+        const int s = (int)(iseq % D);
+        if (lane == 0) {
+          sm.slot_wr[s] = 0;
+          mbar_arrive_expect_tx(&sm.bar[s], (uint32_t)WIN * 4u);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+                  "r"(smem_addr(&sm.ring[s][0])), "l"(&tmx), "r"(0), "r"((int)(base_next >> 5)), "r"(smem_addr(&sm.bar[s]))
+              : "memory");
+        }
+        ++iseq;
+        pre_next = 1;
+      }
+    };
+    int iw = (dbg & 2) ? p1 : skip(pre_here ? WIN : 0);
+    for (int d = (int)pre_here; d < D && iw < p1; ++d) {
       issue(iw);
       iw = skip(iw + WIN);
     }
+    if (can_pre && iw >= p1 && iseq - cseq < (unsigned)D) issue_next();
     int rcur = 0;        // first row overlapping the next window
     double carry = 0.0;  // row rcur's sum before the next window
-    while (cseq != iseq) {
+    while (cseq != iseq - pre_next) {
       const int s = (int)(cseq % D);
       mbar_wait(&sm.bar[s], (phases >> s) & 1u);
       phases ^= 1u << s;
@@ -534,6 +561,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
         }
       }
       if constexpr (SEGF32) {
+        // fp32 range guard: a window holding a finite |v| >= 2^119 could
+        // overflow a 512-term fp32 sum that fp64 would not; such (rare)
+        // windows take the in-order fp64 loop per row below instead
+        float amx = 0.f;
+#pragma unroll
+        for (int k = 0; k < LPL; ++k) amx = fmaxf(amx, fabsf(v[k]));  // NaN ignored, Inf counted
+        const bool big = __any_sync(0xffffffffu, amx >= 0x1p119f && amx <= 3.402823466e38f);
         // ---- pass A: row heads.  Every row starting inside the window marks
         // its first position (empty rows and the block end mark harmlessly:
         // a head only restarts a running sum).
@@ -599,6 +633,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
           float part = sS[LPL * L + (((k >> 2) ^ ((L >> 1) & 3)) << 2) + (k & 3)];
           if (k < __float_as_int(cf.y)) part += cf.x;
           double val = ec > sc ? (double)part : 0.0;
+          if (big) {  // in-order fp64 over the row's part of the window
+            val = 0.0;
+            if (valid)
+              for (int qq = sc; qq < ec; ++qq)
+                val += (double)((wr + qq >= lim4) ? x[base + wr + qq] : sm.ring[s][ring_pos<SWZ>(qq)]);
+          }
           if (s_ < wr) val += carry;  // the row open from the previous window
           const bool complete = valid && e_ <= wend;
           if (complete) sm.res[i] = (RT)val;  // a long row's slot is never flushed
@@ -624,6 +664,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
         if (iw < p1) {
           issue(iw);
           iw = skip(iw + WIN);
+        } else if (can_pre && !pre_next) {
+          issue_next();
         }
       } else {
       // exactness guard: binade span of the window's nonzero magnitudes
@@ -734,6 +776,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
       if (iw < p1) {
         issue(iw);
         iw = skip(iw + WIN);
+      } else if (can_pre && !pre_next) {
+        issue_next();
       }
       }  // exact fp64-prefix windows
     }
@@ -994,7 +1038,7 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaSt
   const int lpl = device_levels(a).l[1]->chunk;
   static int dknob = -1;
   if (dknob < 0) dknob = getenv("HPAR_SEG_D") ? atoi(getenv("HPAR_SEG_D")) : 0;
-  static int f32seg = -1;  // (knob) 1 = fp32 segmented windows (same time, fewer instructions)
+  static int f32seg = -1;  // (knob) 1 = fp32 segmented windows (DESIGN §6 (l), (q))
   if (f32seg < 0) f32seg = getenv("HPAR_SEG_F32") ? atoi(getenv("HPAR_SEG_F32")) : 0;
   auto launch_v = [&](auto lpl_c, auto d_c) -> cudaError_t {
     constexpr int L = decltype(lpl_c)::value, DD = decltype(d_c)::value;

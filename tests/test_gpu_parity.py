@@ -775,3 +775,32 @@ def test_hierarchy_query_cluster_num_is_occupancy(H, torch_mod):
     # the default geometry of a nest is the same single wave
     from paper_2309_01906_b200 import nests
     assert H.Nest(nests.c5_nest(2), device=0, cluster_dim=2, warps_per_cta=8).info().C == nclus
+
+
+def test_segmented_huge_values(H, torch_mod, oracle):
+    """Values near FLT_MAX / 2^9: a window's fp32 segmented sums could
+    overflow where fp64 does not, so windows holding a finite |v| >= 2^119
+    take the in-order fp64 row loop (reading #24).  Rows of such values (sums
+    above FLT_MAX, f64 output) beside rows of tiny and ordinary values,
+    against the oracle's fp64 sums."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    rng = np.random.default_rng(119)
+    rows = 2000
+    lens = np.where(rng.random(rows) < 0.01, rng.integers(4097, 9000, rows), rng.integers(1, 700, rows))
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(off[-1])
+    v = gen.gen_f32(gen.SEED_C3, 0, nnz)
+    kind = rng.integers(0, 3, rows)
+    scale = np.repeat(np.where(kind == 0, 1e37, np.where(kind == 1, 1e-30, 1.0)), lens)
+    v = (v.astype(np.float64) * scale).astype(np.float32)
+    assert np.isfinite(v).all()
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=4)
+    out = torch.full((rows,), -1.0, dtype=torch.float64, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(torch.from_numpy(v).cuda(), out, n0=rows, n1=nnz, nloops=2, keyed=True,
+                                         offsets=torch.from_numpy(off).cuda(), out_dtype=H.F64))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "segmented_csr"
+    want = oracle.segsum_f32(v, off)
+    assert (want[kind == 0] > 3.5e38).any(), "the test needs row sums beyond FLT_MAX"
+    assert_rel(out.cpu().numpy(), want)
