@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
   // cross-block prefetch (SWZ path): once a block has no window left to
   // issue, the next block's first window goes into the free ring slot, so
   // the pipeline does not drain at every block boundary
-  unsigned pre_next = 0;  // windows already issued for the next block (0 / 1)
+  unsigned pre_next = 0;  // windows already issued for the next block (0..2)
   while ((int64_t)u < nblocks) {
     const unsigned pre_here = pre_next;
     pre_next = 0;
@@ -508,22 +508,24 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
     // consumed as a partial window of that row, whose result is never flushed)
     const int64_t base_next = __shfl_sync(0xffffffffu, offr[0], 0) & ~(int64_t)31;
     const bool can_pre = SWZ && (dbg & 64) == 0 && (int64_t)u1 < nblocks;
+    const unsigned xb_max = (dbg & 32) ? 1u : 2u;  // next-block windows issued ahead (knob: HPAR_SEG_DEBUG bit 32 = 1)
     auto issue_next = [&]() {
       if constexpr (SWZ) {
         const int s = (int)(iseq % D);
+        const int w = (int)pre_next * WIN;
         if (lane == 0) {
-          sm.slot_wr[s] = 0;
+          sm.slot_wr[s] = w;
           mbar_arrive_expect_tx(&sm.bar[s], (uint32_t)WIN * 4u);
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-                  "r"(smem_addr(&sm.ring[s][0])), "l"(&tmx), "r"(0), "r"((int)(base_next >> 5)), "r"(smem_addr(&sm.bar[s]))
+                  "r"(smem_addr(&sm.ring[s][0])), "l"(&tmx), "r"(0), "r"((int)((base_next + w) >> 5)), "r"(smem_addr(&sm.bar[s]))
               : "memory");
         }
         ++iseq;
-        pre_next = 1;
+        ++pre_next;
       }
     };
-    int iw = (dbg & 2) ? p1 : skip(pre_here ? WIN : 0);
+    int iw = (dbg & 2) ? p1 : skip((int)pre_here * WIN);
     for (int d = (int)pre_here; d < D && iw < p1; ++d) {
       issue(iw);
       iw = skip(iw + WIN);
@@ -664,7 +666,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
         if (iw < p1) {
           issue(iw);
           iw = skip(iw + WIN);
-        } else if (can_pre && !pre_next) {
+        } else if (can_pre && pre_next < xb_max) {
           issue_next();
         }
       } else {
@@ -776,7 +778,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
       if (iw < p1) {
         issue(iw);
         iw = skip(iw + WIN);
-      } else if (can_pre && !pre_next) {
+      } else if (can_pre && pre_next < xb_max) {
         issue_next();
       }
       }  // exact fp64-prefix windows
