@@ -203,8 +203,9 @@ def run_hpar(args):
         phase = [0]
 
         def step():
-            H.hpar_stencil5(nest, descs[phase[0]], sptr)
-            H.hpar_map_exchange(nest, mspec, bufs[1 - phase[0]], ld, sptr)
+            cs = torch.cuda.current_stream().cuda_stream
+            H.hpar_stencil5(nest, descs[phase[0]], cs)
+            H.hpar_map_exchange(nest, mspec, bufs[1 - phase[0]], ld, cs)
             phase[0] ^= 1
 
         def e2e_step():  # host input -> x, one sweep into out (+ ghost refresh), out -> host
@@ -295,14 +296,18 @@ def run_hpar(args):
     # inputs in L2 and no flush leaves dirty lines to write back during the
     # kernel; larger inputs need neither
     rot_descs = [desc] if step is None else []
+    rot_keep = []  # the copies' tensors: a desc holds raw pointers only
     if step is None and alg_bytes < 3 * L2_BYTES:
         ncopy = min(128, -(-3 * L2_BYTES // max(alg_bytes, 1)) + 1)
         for _ in range(ncopy - 1):
-            rot_descs.append(mk(x.clone(), out.clone(), [t.clone() for t in extra_inputs]))
+            xc, oc, ec = x.clone(), out.clone(), [t.clone() for t in extra_inputs]
+            rot_keep.append((xc, oc, ec))
+            rot_descs.append(mk(xc, oc, ec))
+        assert len({d.in_ for d in rot_descs}) == len(rot_descs), "rotating copies must be distinct buffers"
     rot = [0]
     if step is None:
         def step():
-            nest.parallel_for_reduce(rot_descs[rot[0]], sptr)
+            nest.parallel_for_reduce(rot_descs[rot[0]], torch.cuda.current_stream().cuda_stream)
             rot[0] = (rot[0] + 1) % len(rot_descs)
     if e2e_step is None:
         def e2e_step():
@@ -311,6 +316,30 @@ def run_hpar(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # external=True: inside a graph capture the records become event-record
+    # nodes that timestamp when the graph runs (not capture-time dependencies)
+    ev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+          for _ in range(args.steps)]
+    t_all0 = torch.cuda.Event(enable_timing=True, external=True)
+    t_all1 = torch.cuda.Event(enable_timing=True, external=True)
+
+    def timed_steps():
+        t_all0.record()
+        for i in range(args.steps):
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        t_all1.record()
+
+    graph = None
+    if not args.no_graph:
+        # the K timed steps as ONE CUDA graph, event records included: the
+        # device runs them back to back, so a step's events bracket its
+        # kernel(s), not the host's launch latency (launch-bound configs)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+            timed_steps()
+        torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.15)
@@ -318,15 +347,10 @@ def run_hpar(args):
         dist.barrier()
     torch.cuda.synchronize()
     clocks.mark(0)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    t_all0 = torch.cuda.Event(enable_timing=True)
-    t_all1 = torch.cuda.Event(enable_timing=True)
-    t_all0.record(stream)
-    for i in range(args.steps):
-        ev[i][0].record(stream)
-        step()
-        ev[i][1].record(stream)
-    t_all1.record(stream)
+    if graph is None:
+        timed_steps()
+    else:
+        graph.replay()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -412,6 +436,8 @@ def run_hpar(args):
                      "traffic": traffic, "peak_source": peak_src, "kernel": kernel,
                      "algorithmic_bytes_per_launch": int(alg_bytes)},
         "clocks": clk, "e2e": e2e, "gpu_launches": args.steps,
+        "timing": ("eager launches" if graph is None else f"one CUDA graph of the {args.steps} steps (event records inside)")
+                  + ", CUDA events per step, max over ranks",
     }
     if kind == "hist":  # the second ceiling: shared-memory RED throughput (profiles/r01_red_shared_peak.txt)
         ups = elems_rank / (step_ms_local * 1e-3)
@@ -644,6 +670,7 @@ def main():
     ap.add_argument("--clusters", type=int, default=-1, help="C (0 = resident clusters, -1 = tuned default)")
     ap.add_argument("--warps", type=int, default=0, help="W warps per CTA (0 = tuned default)")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph of K steps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)

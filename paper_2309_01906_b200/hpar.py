@@ -366,6 +366,10 @@ def make_desc(x, out, *, op: int = OP_SUM, n0: int, n1: int = 0, ld: int = 0, nl
     d.global_begin = global_begin
     # local_n0: None = not caller-sharded; a row count (0 = this rank's shard is empty)
     d.local_n0 = 0 if local_n0 is None else (local_n0 if local_n0 > 0 else LOCAL_N0_EMPTY)
+    # the desc holds raw device pointers: keep the tensors alive with it, so a
+    # temporary passed here cannot be freed (and its memory reused) before the
+    # kernel that reads it has run
+    d._keep = (x, out, offsets, list(partials or []), owner, count, fingerprint)
     return d
 
 
@@ -411,6 +415,7 @@ def stencil_desc(inp, out, ld: int, to: Rect, frm: Rect, extent) -> StencilDesc:
     d.in_, d.out, d.ld = inp.data_ptr(), out.data_ptr(), ld
     d.to, d.from_ = to, frm
     d.extent[0], d.extent[1] = extent
+    d._keep = (inp, out)  # raw pointers: keep the tensors alive with the desc
     return d
 
 

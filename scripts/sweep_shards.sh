@@ -2,12 +2,12 @@
 mkdir -p gpurun_out
 for G in 1 2 4 8 16 32 64; do
   for C in -1 296 444; do
-    r=$(timeout -s KILL 120 python bench.py --config c2 --shard $G --clusters $C --steps 200 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step']*1e3,2), 'us', round(d['roofline']['frac'],3), d['config']['geometry'], d['config']['l2'])")
+    r=$(timeout -s KILL 120 python bench.py --config c2 --shard $G --clusters $C --steps 200 --no-cpu-baseline --no-e2e $XARGS 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step']*1e3,2), 'us', round(d['roofline']['frac'],3), d['config']['geometry'], d['config']['l2'])")
     echo "c2 G=$G C=$C $r"
   done
 done
 for G in 1 2 4 8; do
-  r=$(timeout -s KILL 120 python bench.py --config c3 --shard $G --steps 200 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step']*1e3,2), 'us', round(d['roofline']['frac'],3), d['config']['geometry'], d['config']['l2'])")
+  r=$(timeout -s KILL 120 python bench.py --config c3 --shard $G --steps 200 --no-cpu-baseline --no-e2e $XARGS 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step']*1e3,2), 'us', round(d['roofline']['frac'],3), d['config']['geometry'], d['config']['l2'])")
   echo "c3 G=$G $r"
 done
 python - <<'PY'
