@@ -332,7 +332,9 @@ def run_hpar(args):
         t_all1.record()
 
     graph = None
-    if not args.no_graph:
+    # multi-rank runs stay eager (the node level's NCCL call inside a capture is
+    # not exercised on this round's one-GPU boxes; --graph forces it)
+    if not args.no_graph and (world == 1 or args.graph):
         # the K timed steps as ONE CUDA graph, event records included: the
         # device runs them back to back, so a step's events bracket its
         # kernel(s), not the host's launch latency (launch-bound configs)
@@ -671,6 +673,7 @@ def main():
     ap.add_argument("--warps", type=int, default=0, help="W warps per CTA (0 = tuned default)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph of K steps")
+    ap.add_argument("--graph", action="store_true", help="capture the K steps in a CUDA graph also when N > 1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
