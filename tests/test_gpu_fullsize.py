@@ -8,6 +8,8 @@ times (same nests, geometry and kernels):
       partials sum to the bins, sampled ones vs the oracle
   C5  2^34 fp32 (64 GiB): the total vs the oracle's exact sum; coverage
       fingerprints vs the oracle's; sampled cluster partials vs the oracle
+  c6  16384^2 + ghost ring at the 128-byte pitch: two sweeps bit-exact vs
+      the oracle's numpy steps over the whole array
 The oracle runs range by range in a process pool (tests/fullsize_oracle.py:
 every quantity is exact and additive over disjoint ranges).
 Inputs come from the device generator, which is cross-checked bit for bit
@@ -186,3 +188,32 @@ def test_c5_full(env, oracle):
         assert_rel(np.array([cl[c]]), np.array([s * 2.0 ** -24]))
     del x
     torch.cuda.empty_cache()
+
+
+def test_c6_full(env):
+    """c6 (NEXT f3) at bench.py's size and layout: one sibling's 16384^2
+    from-section with its 1-cell ghost ring, rows at the 128-byte pitch
+    (ld = 16416), one Jacobi sweep through hpar_stencil5 — bit-exact against
+    the oracle's numpy step over the whole (16384+2)^2 array, two steps
+    (ping-pong, as timed) likewise."""
+    from oracle import ghostmap as G
+    torch, H, nests, L = env
+    tile = 16384
+    ld = (tile + 2 + 31) // 32 * 32
+    extent = (tile + 2, tile + 2)
+    mspec = H.map_spec(extent, 1, 1, [(tile, 0, tile + 2), (tile, 0, tile + 2)], [(tile, 1, tile), (tile, 1, tile)])
+    H.hpar_map_validate(mspec)
+    to, fr = H.hpar_map_sections(mspec, 0)
+    nest = H.Nest(nests.stencil_nest(), device=0)
+    x = torch.empty((tile + 2, ld), dtype=torch.float32, device="cuda")
+    L.hpar_inputs_fill_f32(gen.SEED_C5, 0, x.numel(), x.data_ptr(), None)
+    out = x.clone()
+    A = x[:, :tile + 2].cpu().numpy()
+    want = G.stencil5_step(A)
+    H.hpar_stencil5(nest, H.stencil_desc(x, out, ld, to, fr, extent))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "stencil5_tma"
+    assert np.array_equal(out[:, :tile + 2].cpu().numpy(), want)
+    H.hpar_stencil5(nest, H.stencil_desc(out, x, ld, to, fr, extent))
+    torch.cuda.synchronize()
+    assert np.array_equal(x[:, :tile + 2].cpu().numpy(), G.stencil5_step(want))
