@@ -185,3 +185,53 @@ def test_shard_range_csr_is_nnz_balanced(H):
                 if rows and nnz:
                     maxlen = int(np.diff(off).max())
                     assert abs(int(off[b + c] - off[b]) - nnz / G) <= maxlen + 1
+
+
+def test_caller_sharded_csr_local_n0(H):
+    """local_n0 (§8(e) C3): rows of a caller-sharded CSR shard; an empty
+    shard (HPAR_LOCAL_N0_EMPTY, what make_desc passes for 0) validates and
+    returns without a launch — never the GPU level's static block of n0 rows
+    with a 1-entry offsets array (ADVICE r01); other negatives are rejected;
+    a non-CSR call with local_n0 is rejected."""
+    import torch
+    from paper_2309_01906_b200 import nests
+    d = H.b200_desc()
+    nest = H.Nest(nests.c3_fast_nest(), device=-1, desc=d, nranks=4, rank=3, cluster_dim=2, warps_per_cta=8,
+                  clusters=4)
+    x = torch.zeros(4, dtype=torch.float32)
+    out = torch.zeros(1, dtype=torch.float32)
+    off = torch.zeros(1, dtype=torch.int64)
+    desc = H.make_desc(x, out, n0=1000, n1=0, nloops=2, keyed=True, offsets=off, local_n0=0)
+    assert desc.local_n0 == H.LOCAL_N0_EMPTY
+    nest.parallel_for_reduce(desc)  # OK: nothing to do on this rank
+    assert nest.last_kernel().startswith("none")
+    desc.local_n0 = -5
+    with pytest.raises(H.HparError) as e:
+        nest.parallel_for_reduce(desc)
+    assert e.value.code == H.HPAR_E_INVALID
+    flat = H.make_desc(x, torch.zeros(1, dtype=torch.float64), n0=4, local_n0=2)
+    with pytest.raises(H.HparError) as e:
+        H.Nest(nests.c5_nest(), device=-1, desc=d).parallel_for_reduce(flat)
+    assert e.value.code == H.HPAR_E_INVALID
+
+
+def test_barrier_levels_host(H):
+    """A10 at host level (reading #26): node / CTA / warp / lane barriers are
+    the kernel boundary, the cluster level has none, the probe is for
+    in-kernel levels only; a describe-only nest cannot execute the GPU-level
+    rendezvous or the probe."""
+    d = H.b200_desc()
+    nest = H.Nest([H.Level(1, 5)], device=-1, desc=d)
+    for lvl in (H.HPAR_CLUSTER,):
+        with pytest.raises(H.HparError) as e:
+            nest.barrier(lvl)
+        assert e.value.code == H.HPAR_E_CAPABILITY
+    with pytest.raises(H.HparError) as e:
+        nest.barrier_probe(H.HPAR_CLUSTER, 0)
+    assert e.value.code == H.HPAR_E_CAPABILITY
+    with pytest.raises(H.HparError) as e:
+        nest.barrier_probe(H.HPAR_GPU, 0)
+    assert e.value.code == H.HPAR_E_INVALID
+    with pytest.raises(H.HparError) as e:
+        nest.barrier(H.HPAR_LANE)
+    assert e.value.code == H.HPAR_E_INVALID and "describe-only" in str(e.value)
