@@ -166,20 +166,22 @@ uint32_t level_props(int level) {
   return 0;
 }
 
-// Grainedness (units unspecified): an ESTIMATE of the SM-cycle
-// cost of one combine/barrier step among the level's siblings.  Not measured
-// on B200: the CTA / warp / lane figures are the B300 (sm_103a) latencies of
-// barrier.cluster, bar.sync and SHFL from B300_MICROARCH.md, the cluster and
-// GPU figures order-of-magnitude kernel-boundary and small-NCCL-allreduce
-// costs.  Only their order (shrinking inward) is relied upon.
+// Grainedness (units unspecified): the SM-cycle cost of one
+// synchronisation / combine step among the level's siblings.  CTA, warp,
+// lane and cluster are MEASURED on B200 (scripts/grain_probe.cu,
+// profiles/r02_grainedness.txt): a dependent SHFL step 30; slot store +
+// bar.sync + sibling load among 8 warps 59; the same over DSMEM with
+// barrier.cluster between 2 CTAs 623; a dependent atom.acq_rel.gpu through
+// L2 (the single-pass ticket clusters meet at) 1495.  GPU and node are
+// estimates (a small NCCL allreduce ~10 us; the job): no multi-GPU box here.
 double level_grain(int level) {
   switch (level) {
-    case HPAR_NODE: return 1e6;
-    case HPAR_GPU: return 2e4;     // NCCL small allreduce ~10 us
-    case HPAR_CLUSTER: return 5e3; // kernel boundary / single pass through L2
-    case HPAR_CTA: return 380;     // barrier.cluster
-    case HPAR_WARP: return 47;     // named bar.sync
-    case HPAR_LANE: return 30;     // SHFL
+    case HPAR_NODE: return 1e6;    // estimate
+    case HPAR_GPU: return 2e4;     // estimate: NCCL 8-byte allreduce ~10 us
+    case HPAR_CLUSTER: return 1495;
+    case HPAR_CTA: return 623;
+    case HPAR_WARP: return 59;
+    case HPAR_LANE: return 30;
   }
   return 1;
 }
