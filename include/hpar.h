@@ -199,6 +199,12 @@ typedef struct {
  * HPAR_E_NCCL).  Applies to total-mode calls; keyed calls have no node
  * level. */
 #define HPAR_NEST_NODE_FUSED 1
+/* HPAR_NEST_NODE_ALWAYS: run the host-enqueued node level (ncclAllReduce /
+ * the ordered ops' allgather + rank fold) and the GPU-level barrier's NCCL
+ * rendezvous even when the communicator has ONE rank, where they are
+ * identities — so the collective path executes on a one-GPU box.  Needs
+ * nccl_comm.  A diagnostic / test option; results are unchanged. */
+#define HPAR_NEST_NODE_ALWAYS 2
 
 typedef struct hpar_nest* hpar_nest_t;
 

@@ -305,6 +305,7 @@ struct hpar_nest {
   bool node_dc_made = false;
   void* node_dc_dev = nullptr;      // device copy of node_dc
   uint64_t node_calls = 0;
+  bool node_always = false;  // HPAR_NEST_NODE_ALWAYS: the node collective also with one rank
 };
 
 namespace {
@@ -560,6 +561,13 @@ extern "C" hpar_status hpar_nest_create(const hpar_nest_level* lv, int32_t nleve
     }
   }
   // ---- fused node level (NEXT f1): collective over the communicator ----
+  if (cfg->flags & HPAR_NEST_NODE_ALWAYS) {
+    if (!n->comm) {
+      hpar_nest_destroy(n);
+      return fail(HPAR_E_INVALID, "HPAR_NEST_NODE_ALWAYS needs an NCCL communicator");
+    }
+    n->node_always = true;
+  }
   if (cfg->flags & HPAR_NEST_NODE_FUSED) {
     hpar_status s = node_fused_setup(n);
     if (s) {
@@ -917,7 +925,7 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   // ---- node level: one allreduce over NVLink (§8(a) A9) ----
   if (node_in_kernel) {
     // done inside the kernel (f1)
-  } else if (!d->keyed && n->nranks > 1 && affine) {
+  } else if (!d->keyed && (n->nranks > 1 || n->node_always) && affine) {
     // an ordered op cannot be an NCCL reduction: gather the per-rank results
     // in rank order (= the GPU level's static-block order) and fold them
     hpar_status s = need_nccl();
@@ -931,7 +939,7 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
     if (r != ncclSuccess) return nccl_fail(r, (ncclComm_t)n->comm, "ncclAllGather");
     e = launch_affine_rank_fold(n->gather_buf, n->nranks, d->out, stream);
     if (e != cudaSuccess) return fail(HPAR_E_CUDA, "rank fold: %s", cudaGetErrorString(e));
-  } else if (!d->keyed && n->nranks > 1) {
+  } else if (!d->keyed && (n->nranks > 1 || n->node_always)) {
     hpar_status s = need_nccl();
     if (s) return s;
     ncclDataType_t t;
@@ -962,7 +970,7 @@ extern "C" hpar_status hpar_barrier(hpar_nest_t n, int32_t level, void* stream_)
   // task of a call has finished (and its writes are visible) at the kernel
   // boundary, which stream order already puts between consecutive calls
   if (level != HPAR_GPU) return ok();
-  if (n->nranks == 1 || !n->comm) return ok();
+  if (!n->comm || (n->nranks == 1 && !n->node_always)) return ok();
   CUDA_TRY(cudaSetDevice(n->device));
   hpar_status s = need_nccl();
   if (s) return s;

@@ -433,6 +433,7 @@ def hpar_map_exchange_local(m: MapSpec, bufs: list, ld: int, stream: int = 0) ->
     _check(lib().hpar_map_exchange_local(ctypes.byref(m), arr, ld, ctypes.c_void_p(stream)))
 
 HPAR_NEST_NODE_FUSED = 1  # hpar_nest_config.flags: the node level inside the kernel (NEXT f1)
+HPAR_NEST_NODE_ALWAYS = 2  # hpar_nest_config.flags: the host node collective also with one rank (tests)
 
 
 def hpar_shard_range_csr(offsets, nranks: int, rank: int) -> tuple[int, int]:

@@ -4,7 +4,10 @@ communicator, LSA stores and barrier.  One GPU here, so the communicator has
 one rank: the slot write / barrier / rank-order fold all run, with G = 1.
 Results must equal the oracle and the host-NCCL path, for every kernel that
 has a node level (flat, hist, teams, generic incl. the ordered AFFINE op),
-over repeated calls (slot halves alternate)."""
+over repeated calls (slot halves alternate).  HPAR_NEST_NODE_ALWAYS runs the
+host-enqueued node level (ncclAllReduce; the ordered op's ncclAllGather +
+rank-fold kernel) and the GPU barrier's NCCL rendezvous through the same
+one-rank communicator: the collective path executes, as an identity."""
 import os
 import socket
 
@@ -47,7 +50,7 @@ def _worker(port, q):
 
         def run(levels, x, op, n0, reps=3, **kw):
             outs = []
-            for flags in (H.HPAR_NEST_NODE_FUSED, 0):
+            for flags in (H.HPAR_NEST_NODE_FUSED, 0, H.HPAR_NEST_NODE_ALWAYS):
                 nest = H.Nest(levels, device=0, nccl_comm=comm, flags=flags, **kw)
                 xd = torch.from_numpy(x).cuda()
                 if op == H.OP_HIST256:
@@ -76,6 +79,11 @@ def _worker(port, q):
         res["generic_affine"] = run([H.Level(1, 3, H.STATIC), H.Level(4, 5, H.STATIC)],
                                     gen.gen_i32(gen.SEED_C1, 0, 70_001).astype(np.int64), H.OP_AFFINE, 70_001,
                                     clusters=2)
+        # the GPU-level barrier's NCCL rendezvous through the same communicator
+        bnest = H.Nest([H.Level(1, 5)], device=0, nccl_comm=comm, flags=H.HPAR_NEST_NODE_ALWAYS)
+        bnest.barrier(H.HPAR_GPU, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        bnest.close()
         q.put(("ok", (res, q_gpu_num)))
         dist.destroy_process_group()
     except Exception as e:  # report, do not hang the parent
@@ -102,10 +110,11 @@ def test_node_level_in_kernel():
         "hist": O.hist256(gen.gen_u8(gen.SEED_C4, 0, n)),
         "generic_min": O.min_i32(gen.gen_i32(gen.SEED_C1, 0, 100_003)),
     }
-    for name, ((k_fused, fused), (k_host, host)) in res.items():
-        assert k_fused == k_host, name
-        for a, b in zip(fused, host):
+    for name, ((k_fused, fused), (k_host, host), (k_coll, coll)) in res.items():
+        assert k_fused == k_host == k_coll, name
+        for a, b, c in zip(fused, host, coll):
             assert np.array_equal(a, b), (name, a, b)   # same kernel, same tree: bit-identical
+            assert np.array_equal(c, b), (name, c, b)   # + the node collective (1 rank: identity)
         if want.get(name) is not None:
             assert np.array_equal(fused[0].astype(np.int64).ravel()[: np.size(want[name])], np.asarray(want[name]).ravel())
     # the ordered op against the oracle (not only fused vs host): block
