@@ -173,7 +173,7 @@ def run_hpar(args):
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     # tuned geometry per config (sweeps in profiles/)
-    tuned = {"c2": (4, 444), "c4": (8, 74)}.get(args.config, (8, 0))
+    tuned = {"c2": (4, 444), "c4": (8, 74), "c5": (4, 148)}.get(args.config, (8, 0))
     K = int(os.environ.get("HPAR_K", "2"))  # CTAs per cluster (knob; 2 = tuned)
     W = args.warps or tuned[0]
     if args.clusters < 0:

@@ -43,7 +43,7 @@ def env():
 
 def bench_geometry(config):
     """the tuned geometry bench.py uses (K, W, C)"""
-    return {"c2": (2, 4, 444), "c4": (2, 8, 74)}.get(config, (2, 8, 0))
+    return {"c2": (2, 4, 444), "c4": (2, 8, 74), "c5": (2, 4, 148)}.get(config, (2, 8, 0))
 
 
 def test_c2_full(env, oracle):
