@@ -173,7 +173,7 @@ def run_hpar(args):
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     # tuned geometry per config (sweeps in profiles/)
-    tuned = {"c2": (4, 444), "c4": (8, 74), "c5": (4, 148)}.get(args.config, (8, 0))
+    tuned = {"c2": (4, 444), "c4": (8, 74), "c5": (4, 148), "c1": (8, 148)}.get(args.config, (8, 0))
     K = int(os.environ.get("HPAR_K", "2"))  # CTAs per cluster (knob; 2 = tuned)
     W = args.warps or tuned[0]
     if args.clusters < 0:
@@ -255,7 +255,10 @@ def run_hpar(args):
         elems_rank = cnt
         host_out_bytes = out.numel() * out.element_size()
     elif kind == "c1":
-        teams = int(os.environ.get("HPAR_C1_TEAMS", "1024"))  # (knob) 0 = resident clusters x K
+        # teams: 0 = C clusters x K CTAs (bench default C = 148: 296 teams of
+        # 3-4 rows, 10.8 us; 1024 teams of one row each: 14.9 us); HPAR_C1_TEAMS
+        # = 1024 is the one-row-per-team form
+        teams = int(os.environ.get("HPAR_C1_TEAMS", "0"))
         nest = H.Nest(nests.c1_nest(outer=teams), device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
                       clusters=args.clusters if teams == 0 else 0,
                       flags=H.HPAR_NEST_NODE_FUSED if (args.node == "fused" and comm is not None) else 0)

@@ -165,12 +165,14 @@ def test_c1_generic_bit_exact(H, torch_mod, oracle):
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     x = gen.gen_i32(gen.SEED_C1, 0, 1 << 20)
-    levels = nests.c1_nest(with_gpu=True)
-    C, K, W = 512, 2, 8
-    res = run_nest(H, torch, levels, x, n0=1024, n1=1024, C=C, K=K, W=W)
-    assert res["out"][0] == oracle.sum_i32(x)
-    assert res["kernel"] == "teams_threads"
-    compare(oracle, H, levels, res, x, n0=1024, n1=1024, C=C, K=K, W=W)
+    # bench.py's launch: 148 clusters x 2 CTAs = 296 teams of 3-4 rows; and
+    # the one-row-per-team form (1024 teams)
+    for levels, C in ((nests.c1_nest(with_gpu=True, outer=0), 148), (nests.c1_nest(with_gpu=True), 512)):
+        K, W = 2, 8
+        res = run_nest(H, torch, levels, x, n0=1024, n1=1024, C=C, K=K, W=W)
+        assert res["out"][0] == oracle.sum_i32(x)
+        assert res["kernel"] == "teams_threads"
+        compare(oracle, H, levels, res, x, n0=1024, n1=1024, C=C, K=K, W=W)
 
 
 SCHEDS = [(0, 0), (1, 1), (1, 3), (1, 8), (3, 0)]
