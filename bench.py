@@ -162,11 +162,15 @@ def run_hpar(args):
     # keyed config (rows are independent: a rank's kernel is exactly this)
     sim_world, sim_rank = world, rank
     shard_kw = {}
+    flat_shard = 1  # c4 / c5: a rank's shard is n0 / G elements of the same kernel
     if args.shard > 1:
-        if world > 1 or args.config not in ("c2", "c3"):
-            raise SystemExit("--shard G: one process, keyed configs (c2, c3) only")
-        sim_world, sim_rank = args.shard, 0
-        shard_kw = dict(nranks=sim_world, rank=sim_rank)
+        if world > 1 or args.config not in ("c2", "c3", "c4", "c5"):
+            raise SystemExit("--shard G: one process, configs c2, c3, c4, c5")
+        if args.config in ("c2", "c3"):
+            sim_world, sim_rank = args.shard, 0
+            shard_kw = dict(nranks=sim_world, rank=sim_rank)
+        else:  # the GPU level is host-applied: rank 0's launch is the nest over its n0 / G elements
+            flat_shard = args.shard
     L = ctypes.CDLL(os.path.join(ROOT, "inputs", "libhpar_inputs.so"))
     for f in ("hpar_inputs_fill_f32", "hpar_inputs_fill_u8", "hpar_inputs_fill_i32"):
         getattr(L, f).argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
@@ -237,7 +241,7 @@ def run_hpar(args):
             nest = H.Nest(nests.c4_nest(K, tile=int(os.environ.get("HPAR_C4_TILE", nests.TILE_U8))),
                           device=local, nccl_comm=comm, cluster_dim=K, warps_per_cta=W,
                           clusters=args.clusters, flags=nflags)
-        b, cnt = nest.shard_range(spec["n0"], rank)
+        b, cnt = nest.shard_range(spec["n0"] // flat_shard, rank)
         if kind == "flat":
             x = torch.empty(cnt, dtype=torch.float32, device=dev)
             L.hpar_inputs_fill_f32(spec["seed"], b, cnt, x.data_ptr(), sptr)
@@ -250,7 +254,8 @@ def run_hpar(args):
             out = torch.empty(256, dtype=torch.int64, device=dev)
             alg_bytes = cnt + 2048
             host_in_bytes = cnt
-        mk = lambda xx, oo, ex: H.make_desc(xx, oo, n0=spec["n0"], op=H.OP_HIST256 if kind == "hist" else H.OP_SUM)
+        mk = lambda xx, oo, ex: H.make_desc(xx, oo, n0=spec["n0"] // flat_shard,
+                                            op=H.OP_HIST256 if kind == "hist" else H.OP_SUM)
         desc = mk(x, out, [])
         elems_rank = cnt
         host_out_bytes = out.numel() * out.element_size()
@@ -668,7 +673,7 @@ def main():
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "c6"])
     ap.add_argument("--check-launch", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--shard", type=int, default=1,
-                    help="diagnostic: time rank 0's shard of a G-GPU run on this one GPU (c2, c3)")
+                    help="diagnostic: time rank 0's shard of a G-GPU run on this one GPU (c2, c3, c4, c5)")
     ap.add_argument("--impl", default="hpar", choices=["hpar", "reference"])
     ap.add_argument("--node", default="nccl", choices=["nccl", "fused"],
                     help="node level of total reductions at N>1: host ncclAllReduce, or in-kernel (NEXT f1)")
