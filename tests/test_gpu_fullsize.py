@@ -10,6 +10,8 @@ times (same nests, geometry and kernels):
       fingerprints vs the oracle's; sampled cluster partials vs the oracle
   c6  16384^2 + ghost ring at the 128-byte pitch: two sweeps bit-exact vs
       the oracle's numpy steps over the whole array
+Edge cases at their stated sizes: C4 with 2^32 equal bytes (bin 0 = 2^32,
+beyond any u32 counter), C3 with one row of 2^26 nonzeros between empty rows.
 The oracle runs range by range in a process pool (tests/fullsize_oracle.py:
 every quantity is exact and additive over disjoint ranges).
 Inputs come from the device generator, which is cross-checked bit for bit
@@ -217,3 +219,42 @@ def test_c6_full(env):
     H.hpar_stencil5(nest, H.stencil_desc(out, x, ld, to, fr, extent))
     torch.cuda.synchronize()
     assert np.array_equal(x[:, :tile + 2].cpu().numpy(), G.stencil5_step(want))
+
+
+def test_c4_full_all_zero(env):
+    """C4's degenerate skew at full size (SURVEY §8(d) skew variants): 2^32
+    equal bytes — every increment lands in bin 0, so bin 0 = 2^32 exactly,
+    which no u32 counter could hold (reading #8: lane / warp / CTA counters
+    stay below 2^32 per task, cluster and GPU bins are u64)."""
+    torch, H, nests, L = env
+    K, W, C = bench_geometry("c4")
+    n = 1 << 32
+    nest = H.Nest(nests.c4_nest(K), device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+    x = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    out = torch.zeros(256, dtype=torch.int64, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=n, op=H.OP_HIST256))
+    torch.cuda.synchronize()
+    bins = out.cpu().numpy().astype(np.uint64)
+    assert int(bins[0]) == n and int(bins[1:].sum()) == 0
+
+
+def test_c3_single_huge_row(env, oracle):
+    """C3's edge case at its stated size: one row of 2^26
+    nonzeros (split into 4096 long-row segments, folded in ascending order by
+    the last one) between empty rows, against the oracle's exact sum (the
+    values are k 2^-24, so the oracle's integer numerator sum is exact)."""
+    torch, H, nests, L = env
+    nnz = 1 << 26
+    off = np.array([0, 0, nnz, nnz, nnz], dtype=np.int64)  # empty, the huge row, two empty
+    x = torch.empty(nnz, dtype=torch.float32, device="cuda")
+    L.hpar_inputs_fill_f32(gen.SEED_C3, 0, nnz, x.data_ptr(), None)
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8)
+    out = torch.full((4,), -1.0, dtype=torch.float64, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=4, n1=nnz, nloops=2, keyed=True,
+                                         offsets=torch.from_numpy(off).cuda(), out_dtype=H.F64))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "segmented_csr"
+    got = out.cpu().numpy()
+    exact = oracle.sum_u64(gen.gen_f32_k(gen.SEED_C3, 0, nnz)) * 2.0 ** -24
+    assert got[0] == 0 and got[2] == 0 and got[3] == 0
+    assert_rel(got[1:2], np.array([exact]))
