@@ -507,7 +507,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
     // yet, so it is window 0 even if that lies inside a long row: then it is
     // consumed as a partial window of that row, whose result is never flushed)
     const int64_t base_next = __shfl_sync(0xffffffffu, offr[0], 0) & ~(int64_t)31;
-    const bool can_pre = SWZ && (dbg & 64) == 0 && (int64_t)u1 < nblocks;
+    // (not with the between-blocks segment serving knob, dbg & 4, whose segments reuse the ring from slot 0)
+    const bool can_pre = SWZ && (dbg & (64 | 4)) == 0 && (int64_t)u1 < nblocks;
     const unsigned xb_max = (dbg & 32) ? 1u : 2u;  // next-block windows issued ahead (knob: HPAR_SEG_DEBUG bit 32 = 1)
     auto issue_next = [&]() {
       if constexpr (SWZ) {
