@@ -806,3 +806,46 @@ def test_segmented_huge_values(H, torch_mod, oracle):
     want = oracle.segsum_f32(v, off)
     assert (want[kind == 0] > 3.5e38).any(), "the test needs row sums beyond FLT_MAX"
     assert_rel(out.cpu().numpy(), want)
+
+
+def test_misaligned_fp32_inputs_not_rejected(H, torch_mod, oracle):
+    """SURVEY §8(b) alignment: an fp32 input 4 bytes off a 16-byte boundary is
+    never rejected — the TMA kernels need 16-byte alignment, so the planner
+    serves such calls with the generic interpreter (P:252 masked lanes) —
+    flat total, dense rows and CSR rows, against the oracle."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    n = 4096 * 2 * 3 + 11
+    x = gen.gen_f32(gen.SEED_C5, 0, n)
+    raw = torch.zeros(n + 8, dtype=torch.float32, device="cuda")
+    xd = raw[1:1 + n]
+    xd.copy_(torch.from_numpy(x).cuda())
+    assert xd.data_ptr() % 16 == 4
+    tot = torch.zeros(1, dtype=torch.float64, device="cuda")
+    nest = H.Nest(nests.c5_nest(2), device=0, cluster_dim=2, warps_per_cta=4, clusters=3)
+    nest.parallel_for_reduce(H.make_desc(xd, tot, n0=n))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "generic"
+    assert_rel(tot.cpu().numpy(), [oracle.sum_f32(x)])
+    rows, cols = 7, 4096
+    a = gen.gen_f32(gen.SEED_C2, 0, rows * cols)
+    raw = torch.zeros(rows * cols + 8, dtype=torch.float32, device="cuda")
+    ad = raw[1:1 + rows * cols]
+    ad.copy_(torch.from_numpy(a).cuda())
+    out = torch.zeros(rows, dtype=torch.float64, device="cuda")
+    nest = H.Nest(nests.c2_nest(), device=0, cluster_dim=2, warps_per_cta=4, clusters=3)
+    nest.parallel_for_reduce(H.make_desc(ad, out, n0=rows, n1=cols, ld=cols, nloops=2, keyed=True, out_dtype=H.F64))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() != "rowwise_tma_dsmem"
+    assert_rel(out.cpu().numpy(), oracle.rowsum_f32(a, rows, cols))
+    off = gen.csr_offsets(300, 5000)
+    v = gen.gen_f32(gen.SEED_C3, 0, 5000)
+    raw = torch.zeros(5008, dtype=torch.float32, device="cuda")
+    vd = raw[1:5001]
+    vd.copy_(torch.from_numpy(v).cuda())
+    out = torch.zeros(300, dtype=torch.float64, device="cuda")
+    nest = H.Nest(nests.c3_nest(rows_chunk=16, width=8), device=0, cluster_dim=2, warps_per_cta=4, clusters=2)
+    nest.parallel_for_reduce(H.make_desc(vd, out, n0=300, nloops=2, keyed=True, offsets=torch.from_numpy(off).cuda(),
+                                         out_dtype=H.F64))
+    torch.cuda.synchronize()
+    assert_rel(out.cpu().numpy(), oracle.segsum_f32(v, off))
