@@ -420,10 +420,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
     __syncwarp();
     load_offs(u1);  // next block's offsets, in flight during this block
     const int p0 = sm.off[0], p1 = sm.off[nr];
-    // long rows: enqueue their segments, mark them, list the first NL
+    // long rows: enqueue their segments, mark them, list the first NL.  A
+    // block spanning <= long_min nonzeros cannot hold one: skip the scan
     int nl = 0;
+    const bool may_long = p1 - p0 > long_min;
+    if (!may_long && lane < RB / 32) sm.lmask[lane] = 0u;
 #pragma unroll
-    for (int k = 0; k < RB / 32; ++k) {
+    for (int k = 0; k < RB / 32 && may_long; ++k) {
       const int i = lane + 32 * k;
       bool lg = false;
       int s_ = 0, e_ = 0;
