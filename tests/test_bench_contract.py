@@ -10,7 +10,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("config", ["c1", "c2", "c6"])
+@pytest.mark.parametrize("config", ["c1", "c2", "c6", "c5"])
 def test_reference_arm_line(config):
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", config, "--steps", "1",
                         "--warmup", "1"], cwd=ROOT, capture_output=True, text=True, timeout=600)
