@@ -849,3 +849,23 @@ def test_misaligned_fp32_inputs_not_rejected(H, torch_mod, oracle):
                                          out_dtype=H.F64))
     torch.cuda.synchronize()
     assert_rel(out.cpu().numpy(), oracle.segsum_f32(v, off))
+
+
+def test_rowwise_padded_rows(H, torch_mod, oracle):
+    """Dense rows with a row stride larger than the row (ld > n1, 16-byte
+    multiples): the fused row-wise kernel reads only the n1 columns of each
+    row; rows, owner map and per-level partials against the oracle (whose
+    nest walk takes the same ld)."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c2_nest()
+    for n0, n1, ld, C in ((37, 4096, 4096 + 64, 5), (11, 2048, 3000 + 4, 3)):
+        a = gen.gen_f32(gen.SEED_C2, 0, n0 * ld).reshape(n0, ld)
+        a[:, n1:] = np.float32(np.nan)  # the padding must never be read
+        x = torch.from_numpy(a.ravel().copy()).cuda()
+        out = torch.zeros(n0, dtype=torch.float64, device="cuda")
+        nest = H.Nest(levels, device=0, cluster_dim=2, warps_per_cta=4, clusters=C)
+        nest.parallel_for_reduce(H.make_desc(x, out, n0=n0, n1=n1, ld=ld, nloops=2, keyed=True, out_dtype=H.F64))
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "rowwise_tma_dsmem"
+        assert_rel(out.cpu().numpy(), oracle.rowsum_f32(np.ascontiguousarray(a[:, :n1]), n0, n1))
