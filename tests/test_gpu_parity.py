@@ -854,8 +854,8 @@ def test_misaligned_fp32_inputs_not_rejected(H, torch_mod, oracle):
 def test_rowwise_padded_rows(H, torch_mod, oracle):
     """Dense rows with a row stride larger than the row (ld > n1, 16-byte
     multiples): the fused row-wise kernel reads only the n1 columns of each
-    row; rows, owner map and per-level partials against the oracle (whose
-    nest walk takes the same ld)."""
+    row (the padding holds NaN, which would poison any row that read it);
+    row sums against the oracle's."""
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     levels = nests.c2_nest()
