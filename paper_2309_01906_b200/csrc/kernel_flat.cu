@@ -27,7 +27,25 @@ namespace {
 
 constexpr int kStages = 4;
 
-template <typename In, typename Acc, int OP, bool VERIFY>
+// ring stage stride: a misaligned input (4, 8 or 12 bytes past a 16-byte
+// granule) copies the enclosing granules, one more than the aligned tile
+__host__ __device__ __forceinline__ uint32_t stage_stride(uint32_t tile_bytes, bool mis) {
+  return mis ? tile_bytes + 16 : tile_bytes;
+}
+
+// elements m4 .. m4+3 of the 8-element concatenation (a, b), m4 in 1..3
+// (warp-uniform): the 16-byte vector of a lane when the tile starts m4
+// elements into its first granule
+template <typename V>
+__device__ __forceinline__ V shift4(const V& a, const V& b, uint32_t m4) {
+  V r;
+  if (m4 == 1) { r.x = a.y; r.y = a.z; r.z = a.w; r.w = b.x; }
+  else if (m4 == 2) { r.x = a.z; r.y = a.w; r.z = b.x; r.w = b.y; }
+  else { r.x = a.w; r.y = b.x; r.z = b.y; r.w = b.z; }
+  return r;
+}
+
+template <typename In, typename Acc, int OP, bool VERIFY, bool MIS>
 __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant__ NestArgs a, int W,
                                                             int tile) {
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -42,6 +60,10 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
   const int64_t my_tiles = (b < ntiles) ? (ntiles - 1 - b) / nblocks + 1 : 0;
   const In* x = (const In*)a.in;
   const uint32_t tile_bytes = (uint32_t)tile * sizeof(In);
+  // misaligned input (P:252's peel, done by the copy): the ring holds the
+  // granules enclosing each tile, whose elements then start at byte `mis`
+  const uint32_t mis = MIS ? (uint32_t)((uintptr_t)x & 15) : 0u;
+  const uint32_t stride = stage_stride(tile_bytes, MIS);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -63,9 +85,13 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
         const int64_t t = j * nblocks + b;
         const int64_t base = t * tile;
         const int64_t len = (n - base < tile) ? (n - base) : tile;
-        const uint32_t bytes = (uint32_t)((len * sizeof(In)) & ~(int64_t)15);  // TMA: multiple of 16 B
+        // TMA: multiple of 16 B; a misaligned tile takes its enclosing
+        // granules (never past the granule of a valid element)
+        const uint32_t bytes = MIS ? (uint32_t)((len * (int64_t)sizeof(In) + mis + 15) & ~(int64_t)15)
+                                   : (uint32_t)((len * sizeof(In)) & ~(int64_t)15);
         mbar_arrive_expect_tx(&full[s], bytes);
-        if (bytes) bulk_g2s(dsm + (size_t)s * tile_bytes, x + base, bytes, &full[s], pol);
+        if (bytes)
+          bulk_g2s(dsm + (size_t)s * stride, (const unsigned char*)(x + base) - mis, bytes, &full[s], pol);
       }
     }
   } else {
@@ -79,9 +105,41 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
       const int64_t base = t * tile;
       const int64_t len = (n - base < tile) ? (n - base) : tile;
       mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
-      const In* st = (const In*)(dsm + (size_t)s * tile_bytes);
+      const In* st = (const In*)(dsm + (size_t)s * stride + mis);
       if (len == tile) {
-        if constexpr (sizeof(In) == 4) {
+        if constexpr (sizeof(In) == 4 && MIS) {
+          // two aligned LDS.128 per vector (conflict-free) and a uniform
+          // shift: the same four elements, the same arithmetic as below
+          using V = typename std::conditional<std::is_floating_point<In>::value, float4, int4>::type;
+          const V* g = (const V*)(dsm + (size_t)s * stride);
+          const uint32_t m4 = mis / 4;
+#pragma unroll 4
+          for (int f = warp * 32 + lane; f < vec_per_tile; f += W * 32) {
+            const V v = shift4(g[f], g[f + 1], m4);
+            if constexpr (OP == OP_SUM) {
+              if constexpr (std::is_floating_point<Acc>::value) {
+                acc += (double)((v.x + v.y) + (v.z + v.w));
+              } else {
+                acc += (long long)v.x + (long long)v.y + (long long)v.z + (long long)v.w;
+              }
+            } else {
+              acc = OpT<OP, Acc>::combine(acc, (Acc)v.x);
+              acc = OpT<OP, Acc>::combine(acc, (Acc)v.y);
+              acc = OpT<OP, Acc>::combine(acc, (Acc)v.z);
+              acc = OpT<OP, Acc>::combine(acc, (Acc)v.w);
+            }
+            if constexpr (VERIFY) {
+              for (int q = 0; q < 4; ++q) {
+                const int64_t it = base + 4 * f + q;
+                if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
+                if (a.verify & V_FINGERPRINT) {
+                  const uint64_t g2 = a.global_begin + (uint64_t)it;
+                  fpo += fp_mix(g2); fpw += fp_mix2(g2, (uint64_t)leaf); fpn += 1;
+                }
+              }
+            }
+          }
+        } else if constexpr (sizeof(In) == 4) {
 #pragma unroll 4
           for (int f = warp * 32 + lane; f < vec_per_tile; f += W * 32) {
             if constexpr (OP == OP_SUM) {
@@ -113,7 +171,7 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
         }
       } else {
         // ragged last tile: bulk part from smem, the < 16 B tail from global
-        const int64_t in_smem = (len * (int64_t)sizeof(In)) / 16 * 16 / (int64_t)sizeof(In);
+        const int64_t in_smem = MIS ? len : (len * (int64_t)sizeof(In)) / 16 * 16 / (int64_t)sizeof(In);
         for (int f = warp * 32 + lane; f < vec_per_tile; f += W * 32) {
           for (int q = 0; q < 4; ++q) {
             const int64_t off = 4 * (int64_t)f + q;
@@ -148,10 +206,10 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
 
 int g_flat_tile = 4096;
 
-template <typename In, typename Acc, int OP, bool VERIFY>
+template <typename In, typename Acc, int OP, bool VERIFY, bool MIS>
 cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
-  auto kern = flat_tma_kernel<In, Acc, OP, VERIFY>;
-  const size_t smem = (size_t)kStages * tile * sizeof(In);
+  auto kern = flat_tma_kernel<In, Acc, OP, VERIFY, MIS>;
+  const size_t smem = (size_t)kStages * stage_stride((uint32_t)(tile * sizeof(In)), MIS);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -171,7 +229,9 @@ cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
 
 template <typename In, typename Acc, int OP>
 cudaError_t launch_v(const NestArgs& a, int W, int tile, cudaStream_t s) {
-  return a.verify ? launch_t<In, Acc, OP, true>(a, W, tile, s) : launch_t<In, Acc, OP, false>(a, W, tile, s);
+  if (((uintptr_t)a.in & 15) != 0)
+    return a.verify ? launch_t<In, Acc, OP, true, true>(a, W, tile, s) : launch_t<In, Acc, OP, false, true>(a, W, tile, s);
+  return a.verify ? launch_t<In, Acc, OP, true, false>(a, W, tile, s) : launch_t<In, Acc, OP, false, false>(a, W, tile, s);
 }
 
 }  // namespace
@@ -181,7 +241,7 @@ bool flat_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 1 || a.keyed) { *why = "not a flat total"; return false; }
   if (a.op == OP_HIST || a.op == OP_AFFINE) { *why = "sum/min/max only"; return false; }
   if (a.in_dtype != DT_F32 && a.in_dtype != DT_I32) { *why = "dtype"; return false; }
-  if (((uintptr_t)a.in & 15) != 0) { *why = "input not 16-byte aligned"; return false; }
+  if (((uintptr_t)a.in & 3) != 0) { *why = "input not element-aligned"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
   LevelView v = device_levels(a);
   if (v.n != 4) { *why = "needs cluster, CTA, warp, lane levels"; return false; }
@@ -224,7 +284,7 @@ cudaError_t launch_flat(const NestArgs& a, int W, cudaStream_t s, const char** n
 // (cudaOccupancyMaxActiveClusters: counts SMs, per-SM residency and the GPC
 // placement of clusters).  0 on error.
 int flat_max_active_clusters(int K, int W) {
-  auto kern = flat_tma_kernel<float, double, OP_SUM, false>;
+  auto kern = flat_tma_kernel<float, double, OP_SUM, false, false>;
   const size_t smem = (size_t)kStages * g_flat_tile * 4;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
   if (K > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return 0;
@@ -246,7 +306,7 @@ int flat_max_active_clusters(int K, int W) {
 
 int flat_resident_ctas_per_sm(int W) {
   int n = 0;
-  auto kern = flat_tma_kernel<float, double, OP_SUM, false>;
+  auto kern = flat_tma_kernel<float, double, OP_SUM, false, false>;
   const size_t smem = (size_t)kStages * g_flat_tile * 4;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 2;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, (W + 1) * 32, smem) != cudaSuccess || n < 1) return 2;

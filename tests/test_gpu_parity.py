@@ -70,9 +70,10 @@ def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, 
         n_iter = n0 * (n1 if nloops == 2 else 1)
     xd = torch.from_numpy(x).cuda()
     if misalign:  # the input starts `misalign` bytes past a 16-byte boundary
-        assert x.dtype == np.uint8
-        raw = torch.zeros(x.size + 32, dtype=torch.uint8, device="cuda")
-        xd = raw[misalign:misalign + x.size]
+        assert misalign % x.itemsize == 0
+        e0 = misalign // x.itemsize
+        raw = torch.zeros(x.size + 32, dtype=xd.dtype, device="cuda")
+        xd = raw[e0:e0 + x.size]
         xd.copy_(torch.from_numpy(x).cuda())
         assert xd.data_ptr() % 16 == misalign
     fp = x.dtype.kind == "f"
@@ -307,6 +308,32 @@ def test_flat_fused_kernel(H, torch_mod, oracle, n):
     xi = gen.gen_i32(gen.SEED_C1, 0, n)
     res = run_nest(H, torch, levels, xi, n0=n, C=C, K=K, W=W, coverage=False, partials=False)
     assert res["out"][0] == oracle.sum_i32(xi)
+
+
+@pytest.mark.parametrize("mis", [4, 8, 12])
+def test_flat_misaligned_input(H, torch_mod, oracle, mis):
+    """An fp32/int32 input 4, 8 or 12 bytes off a 16-byte boundary stays on
+    the fused flat kernel (SURVEY §8(b) alignment; P:252's peel done by the
+    copy): tiles copy their enclosing granules and each lane takes its four
+    elements from two aligned vectors.  Total, owner map (the nominal static
+    closed form) and every level's partials vs the oracle; the int32 total
+    exact; the fp32 total bitwise equal to the aligned call's (same owner
+    map, same arithmetic order)."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c5_nest(K=2)
+    C, K, W = 5, 2, 8
+    for n in (1, 3, 7, 4096 * 2 * 5, 4096 * 2 * 7 + 4 * 99 + 3, 300001):
+        x = gen.gen_f32(gen.SEED_C5, 0, n)
+        res = run_nest(H, torch, levels, x, n0=n, C=C, K=K, W=W, misalign=mis)
+        assert res["kernel"] == "flat_tma"
+        compare(oracle, H, levels, res, x, n0=n, C=C, K=K, W=W)
+        ref = run_nest(H, torch, levels, x, n0=n, C=C, K=K, W=W, coverage=False, partials=False)
+        assert res["out"].tobytes() == ref["out"].tobytes()
+        xi = gen.gen_i32(gen.SEED_C1, 0, n)
+        res = run_nest(H, torch, levels, xi, n0=n, C=C, K=K, W=W, coverage=False, partials=False, misalign=mis)
+        assert res["kernel"] == "flat_tma"
+        assert res["out"][0] == oracle.sum_i32(xi)
 
 
 def test_rowwise_fused_kernel_small(H, torch_mod, oracle):
@@ -810,9 +837,11 @@ def test_segmented_huge_values(H, torch_mod, oracle):
 
 def test_misaligned_fp32_inputs_not_rejected(H, torch_mod, oracle):
     """SURVEY §8(b) alignment: an fp32 input 4 bytes off a 16-byte boundary is
-    never rejected — the TMA kernels need 16-byte alignment, so the planner
-    serves such calls with the generic interpreter (P:252 masked lanes) —
-    flat total, dense rows and CSR rows, against the oracle."""
+    never rejected — the flat kernel copies enclosing granules
+    (test_flat_misaligned_input); the row-wise TMA kernel needs 16-byte
+    aligned rows, so the planner serves those calls with the generic
+    interpreter (P:252 masked lanes) — flat total, dense rows and CSR rows,
+    against the oracle."""
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     n = 4096 * 2 * 3 + 11
@@ -825,7 +854,7 @@ def test_misaligned_fp32_inputs_not_rejected(H, torch_mod, oracle):
     nest = H.Nest(nests.c5_nest(2), device=0, cluster_dim=2, warps_per_cta=4, clusters=3)
     nest.parallel_for_reduce(H.make_desc(xd, tot, n0=n))
     torch.cuda.synchronize()
-    assert nest.last_kernel() == "generic"
+    assert nest.last_kernel() == "flat_tma"
     assert_rel(tot.cpu().numpy(), [oracle.sum_f32(x)])
     rows, cols = 7, 4096
     a = gen.gen_f32(gen.SEED_C2, 0, rows * cols)
