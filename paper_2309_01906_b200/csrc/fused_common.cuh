@@ -35,6 +35,18 @@ inline bool is_level(const DevLevel* L, int hw_slot) {
 
 // Write the partial of the task at `slot` to every nest level whose last
 // slot is `slot` (verify mode).  `index` = task id below the GPU.
+// elements m4 .. m4+3 of the 8-element concatenation (a, b), m4 in 1..3
+// (warp-uniform): a lane's 4-element vector when the copied granules start
+// m4 elements before the data (misaligned inputs, ragged rows)
+template <typename V>
+__device__ __forceinline__ V shift4(const V& a, const V& b, uint32_t m4) {
+  V r;
+  if (m4 == 1) { r.x = a.y; r.y = a.z; r.z = a.w; r.w = b.x; }
+  else if (m4 == 2) { r.x = a.z; r.y = a.w; r.z = b.x; r.w = b.y; }
+  else { r.x = a.w; r.y = b.x; r.z = b.y; r.w = b.z; }
+  return r;
+}
+
 template <typename Acc>
 __device__ __forceinline__ void export_slot(const NestArgs& a, int slot, int64_t index, Acc v) {
   if (!(a.verify & V_PARTIALS)) return;

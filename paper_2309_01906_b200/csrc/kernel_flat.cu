@@ -33,18 +33,6 @@ __host__ __device__ __forceinline__ uint32_t stage_stride(uint32_t tile_bytes, b
   return mis ? tile_bytes + 16 : tile_bytes;
 }
 
-// elements m4 .. m4+3 of the 8-element concatenation (a, b), m4 in 1..3
-// (warp-uniform): the 16-byte vector of a lane when the tile starts m4
-// elements into its first granule
-template <typename V>
-__device__ __forceinline__ V shift4(const V& a, const V& b, uint32_t m4) {
-  V r;
-  if (m4 == 1) { r.x = a.y; r.y = a.z; r.z = a.w; r.w = b.x; }
-  else if (m4 == 2) { r.x = a.z; r.y = a.w; r.z = b.x; r.w = b.y; }
-  else { r.x = a.w; r.y = b.x; r.z = b.y; r.w = b.z; }
-  return r;
-}
-
 template <typename In, typename Acc, int OP, bool VERIFY, bool MIS>
 __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant__ NestArgs a, int W,
                                                             int tile) {

@@ -42,7 +42,28 @@ constexpr int kSlots = 16;      // DSMEM row-slot ring depth in the leader
 constexpr int kMaxPush = 32;    // K*W <= 32 warp partials per row
 
 
-// NV: float4 vectors per lane per row (qcols == 128*W*NV); 0 = generic loop
+// NV: float4 vectors per lane per row (qcols == 128*W*NV); 0 = generic loop;
+// -1 = ragged rows: any n1, ld and 4-byte aligned input.  Then the CTAs'
+// column blocks follow the static partition (the first n1 % K CTAs take one
+// column more), a CTA's segment of a row may start anywhere in a 16-byte
+// granule, so the producer copies the enclosing granules and the lanes shift
+// (shift4) by the row's offset; qcols is the ring-stage stride in floats.
+bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// rows the aligned path cannot copy whole: n1 not a multiple of 4K, or rows
+// (ld, the base pointer) off 16-byte boundaries
+bool rowwise_ragged(const NestArgs& a) {
+  return a.n1 % (4 * a.K) != 0 || a.ld % 4 != 0 || ((uintptr_t)a.in & 15) != 0;
+}
+
+// ring-stage stride in floats: the aligned path's n1/K; a ragged segment of up
+// to ceil(n1/K) columns starting anywhere in a granule needs one granule more
+int rowwise_stride(const NestArgs& a) {
+  if (!rowwise_ragged(a)) return (int)(a.n1 / a.K);
+  const int64_t qmax = (a.n1 + a.K - 1) / a.K;
+  return (int)(((qmax + 3) / 4 + 1) * 4);
+}
+
 template <bool VERIFY, int NV>
 __global__ void __launch_bounds__(1024, 1)
     rowwise_kernel(const __grid_constant__ NestArgs a, int W, int qcols, int kStages) {
@@ -59,7 +80,9 @@ __global__ void __launch_bounds__(1024, 1)
   const int64_t q = a.n0 / a.C, r = a.n0 % a.C;
   const int64_t row0 = c * q + (c < r ? c : r);
   const uint32_t nrows = (uint32_t)(q + (c < r ? 1 : 0));
-  const int64_t col0 = (int64_t)crank * qcols;
+  const int64_t q1 = a.n1 / K, r1 = a.n1 % K;
+  const int64_t col0 = NV < 0 ? (int64_t)crank * q1 + ((int64_t)crank < r1 ? crank : r1) : (int64_t)crank * qcols;
+  const int lenk = NV < 0 ? (int)(q1 + ((int64_t)crank < r1 ? 1 : 0)) : qcols;  // this CTA's columns
   const float* x = (const float*)a.in;
   const uint32_t seg_bytes = (uint32_t)qcols * 4;
   const int npush = K * W;
@@ -86,8 +109,17 @@ __global__ void __launch_bounds__(1024, 1)
       uint32_t ph = 0;
       for (uint32_t j = 0; j < nrows; ++j) {
         if (j >= (uint32_t)kStages) mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], seg_bytes);
-        bulk_g2s(dsm + (size_t)s * seg_bytes, src, seg_bytes, &full[s], pol);
+        if constexpr (NV < 0) {
+          // the granules enclosing this row's segment (never past the
+          // granule of a valid element)
+          const uint32_t mis = (uint32_t)((uintptr_t)src & 15);
+          const uint32_t bytes = lenk ? (uint32_t)((lenk * 4 + mis + 15) & ~15u) : 0u;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          if (bytes) bulk_g2s(dsm + (size_t)s * seg_bytes, (const unsigned char*)src - mis, bytes, &full[s], pol);
+        } else {
+          mbar_arrive_expect_tx(&full[s], seg_bytes);
+          bulk_g2s(dsm + (size_t)s * seg_bytes, src, seg_bytes, &full[s], pol);
+        }
         src += a.ld;
         if (++s == kStages) { s = 0; ph ^= 1; }
       }
@@ -126,7 +158,7 @@ __global__ void __launch_bounds__(1024, 1)
     }
   } else {
     // ------------------------------ W consumer warps --------------------
-    const int nvec = qcols / 4;
+    const int nvec = NV < 0 ? (lenk + 3) / 4 : qcols / 4;
     const uint32_t leader_slot_base = mapa(smem_addr(&slot[0][0]), 0);
     const uint32_t leader_full_base = mapa(smem_addr(&row_full[0]), 0);
     const int push_idx = (int)crank * W + warp;
@@ -143,6 +175,19 @@ __global__ void __launch_bounds__(1024, 1)
           const float4 t = st[(v * W + warp) * 32 + lane];
           acc += (t.x + t.y) + (t.z + t.w);
         }
+      } else if constexpr (NV < 0) {
+        const uint32_t m4 = (uint32_t)((((uintptr_t)(x + (row0 + j) * a.ld + col0)) & 15) >> 2);
+        for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
+          float4 t = st[f];
+          if (m4) t = shift4(t, st[f + 1], m4);
+          const int rem = lenk - 4 * f;  // the last vector may be partial: zeros keep the tree's order
+          if (rem < 4) {
+            t.w = 0.f;
+            if (rem < 3) t.z = 0.f;
+            if (rem < 2) t.y = 0.f;
+          }
+          acc += (t.x + t.y) + (t.z + t.w);
+        }
       } else {
         for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
           const float4 t = st[f];
@@ -151,7 +196,7 @@ __global__ void __launch_bounds__(1024, 1)
       }
       if constexpr (VERIFY) {
         for (int f = warp * 32 + lane; f < nvec; f += W * 32)
-          for (int e = 0; e < 4; ++e) {
+          for (int e = 0; e < 4 && 4 * f + e < lenk; ++e) {
             const int64_t it = (row0 + j) * a.n1 + col0 + 4 * f + e;
             if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
           }
@@ -206,6 +251,7 @@ cudaError_t launch_t(const NestArgs& a, int W, int qcols, int stages, cudaStream
 
 template <bool V>
 cudaError_t launch_nv(const NestArgs& a, int W, int qcols, int stages, cudaStream_t s) {
+  if (rowwise_ragged(a)) return launch_t<V, -1>(a, W, qcols, stages, s);
   const int nv = (qcols % (128 * W) == 0) ? qcols / (128 * W) : 0;
   switch (nv) {
     case 1: return launch_t<V, 1>(a, W, qcols, stages, s);
@@ -216,7 +262,6 @@ cudaError_t launch_nv(const NestArgs& a, int W, int qcols, int stages, cudaStrea
   }
 }
 
-bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
 int rowwise_stages(int qcols) {
   static int env = -2;
@@ -253,15 +298,15 @@ bool rowwise_matches(const NestArgs& a, const char** why) {
   if (l->loop != 1 || l->sched != SCHED_STATIC_CHUNK || l->chunk != 4) { *why = "lane static(4)"; return false; }
   const int64_t K = a.K, W = a.radix[S_WARP];
   if (!pow2(K) || !pow2(W) || K * W > kMaxPush || W > 30) { *why = "K, W powers of two, K*W <= 32"; return false; }
-  if (a.n1 % (4 * K) != 0 || a.ld % 4 != 0 || ((uintptr_t)a.in & 15)) { *why = "alignment"; return false; }
-  if ((a.n1 / K) * 4 * 2 > 200 * 1024) { *why = "row segment too large for the smem ring"; return false; }
+  if (((uintptr_t)a.in & 3) || a.ld < a.n1) { *why = "input not element-aligned or ld < n1"; return false; }
+  if ((int64_t)rowwise_stride(a) * 4 * 2 > 200 * 1024) { *why = "row segment too large for the smem ring"; return false; }
   if (a.n1 == 0) { *why = "empty rows"; return false; }
   return true;
 }
 
 cudaError_t launch_rowwise(const NestArgs& a, int W, cudaStream_t s, const char** name) {
   *name = "rowwise_tma_dsmem";
-  const int qcols = (int)(a.n1 / a.K);
+  const int qcols = rowwise_stride(a);
   const int st = rowwise_stages(qcols);
   return a.verify ? launch_nv<true>(a, W, qcols, st, s) : launch_nv<false>(a, W, qcols, st, s);
 }

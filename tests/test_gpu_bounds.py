@@ -103,7 +103,7 @@ def test_flat_and_teams_bounds(env, oracle):
 
 def test_rowwise_bounds(env, oracle):
     torch, H, nests = env
-    for rows, cols in ((37, 4096), (5, 1000)):
+    for rows, cols in ((37, 4096), (5, 1000), (11, 1003), (3, 5)):  # the last two: ragged (granule) copies
         a = gen.gen_f32(gen.SEED_C2, 0, rows * cols)
         _, ad = poisoned_input(torch, a)
         nest = H.Nest(nests.c2_nest(), device=0, cluster_dim=2, warps_per_cta=4, clusters=7)

@@ -61,7 +61,7 @@ def test_device_generator_matches_numpy(inputs_lib, torch_mod):
 
 # ---------------------------------------------------------------------------
 def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, C=4, K=2, W=4,
-             partials=True, coverage=True, max_inner=0, out_f64=True, misalign=0):
+             partials=True, coverage=True, max_inner=0, out_f64=True, misalign=0, ld=0):
     nest = H.Nest(levels, device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
     nloops = 2 if (n1 or offsets is not None) else 1
     if offsets is not None:
@@ -69,12 +69,20 @@ def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, 
     else:
         n_iter = n0 * (n1 if nloops == 2 else 1)
     xd = torch.from_numpy(x).cuda()
+    if ld and ld != n1:  # rows at stride ld; the padding columns hold NaN (a read of them poisons the row)
+        assert nloops == 2 and ld > n1 and x.dtype == np.float32
+        xp = np.full((n0, ld), np.nan, dtype=np.float32)
+        xp[:, :n1] = x.reshape(n0, n1)
+        x_dev_src = xp.reshape(-1)
+    else:
+        x_dev_src = x
+    xd = torch.from_numpy(x_dev_src).cuda()
     if misalign:  # the input starts `misalign` bytes past a 16-byte boundary
         assert misalign % x.itemsize == 0
         e0 = misalign // x.itemsize
-        raw = torch.zeros(x.size + 32, dtype=xd.dtype, device="cuda")
-        xd = raw[e0:e0 + x.size]
-        xd.copy_(torch.from_numpy(x).cuda())
+        raw = torch.zeros(x_dev_src.size + 32, dtype=xd.dtype, device="cuda")
+        xd = raw[e0:e0 + x_dev_src.size]
+        xd.copy_(torch.from_numpy(x_dev_src).cuda())
         assert xd.data_ptr() % 16 == misalign
     fp = x.dtype.kind == "f"
     if op == H.OP_AFFINE:
@@ -110,7 +118,7 @@ def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, 
                                     device="cuda"))
     offs = torch.from_numpy(offsets).cuda() if offsets is not None else None
     verify = (H.VERIFY_COVERAGE if coverage else 0) | (H.VERIFY_PARTIALS if partials else 0)
-    d = H.make_desc(xd, out, op=op, n0=n0, n1=n1, ld=n1, nloops=nloops, keyed=keyed, offsets=offs,
+    d = H.make_desc(xd, out, op=op, n0=n0, n1=n1, ld=ld or n1, nloops=nloops, keyed=keyed, offsets=offs,
                     max_inner=max_inner, verify=verify, partials=parts, owner=owner, count=count,
                     out_dtype=(H.U64 if op == H.OP_AFFINE else (H.F64 if fp else H.I64)) if keyed else -1)
     nest.parallel_for_reduce(d)
@@ -334,6 +342,26 @@ def test_flat_misaligned_input(H, torch_mod, oracle, mis):
         res = run_nest(H, torch, levels, xi, n0=n, C=C, K=K, W=W, coverage=False, partials=False, misalign=mis)
         assert res["kernel"] == "flat_tma"
         assert res["out"][0] == oracle.sum_i32(xi)
+
+
+@pytest.mark.parametrize("n0,n1,ld,mis", [(50, 4095, 4095, 0), (37, 4100, 4100, 0), (29, 4092, 4092, 8),
+                                          (40, 4096, 4096, 4), (33, 4095, 4096, 0), (21, 1001, 1003, 12),
+                                          (9, 3, 5, 4), (6, 1, 1, 0), (300, 777, 777, 0)])
+def test_rowwise_ragged_rows(H, torch_mod, oracle, n0, n1, ld, mis):
+    """Rows the aligned copy cannot take whole — n1 not a multiple of 4K,
+    ld not a multiple of 4 (NaN padding columns), the base pointer off a
+    16-byte boundary — stay on the fused row-wise kernel: each CTA copies the
+    granules enclosing its static column block of the row and its lanes
+    shift by the row's offset.  Rows, owner map and every level's partials
+    vs the oracle."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c2_nest()
+    for K, W, C in ((2, 4, 7), (4, 8, 3)):
+        x = gen.gen_f32(gen.SEED_C2, 0, n0 * n1)
+        res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=True, C=C, K=K, W=W, ld=ld, misalign=mis)
+        assert res["kernel"] == "rowwise_tma_dsmem"
+        compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, C=C, K=K, W=W)
 
 
 def test_rowwise_fused_kernel_small(H, torch_mod, oracle):
@@ -837,11 +865,10 @@ def test_segmented_huge_values(H, torch_mod, oracle):
 
 def test_misaligned_fp32_inputs_not_rejected(H, torch_mod, oracle):
     """SURVEY §8(b) alignment: an fp32 input 4 bytes off a 16-byte boundary is
-    never rejected — the flat kernel copies enclosing granules
-    (test_flat_misaligned_input); the row-wise TMA kernel needs 16-byte
-    aligned rows, so the planner serves those calls with the generic
-    interpreter (P:252 masked lanes) — flat total, dense rows and CSR rows,
-    against the oracle."""
+    never rejected — the flat and row-wise kernels copy enclosing granules
+    (test_flat_misaligned_input, test_rowwise_ragged_rows); the CSR rows of
+    the generic nest go to the interpreter (P:252 masked lanes) — flat
+    total, dense rows and CSR rows, against the oracle."""
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     n = 4096 * 2 * 3 + 11
@@ -865,7 +892,7 @@ def test_misaligned_fp32_inputs_not_rejected(H, torch_mod, oracle):
     nest = H.Nest(nests.c2_nest(), device=0, cluster_dim=2, warps_per_cta=4, clusters=3)
     nest.parallel_for_reduce(H.make_desc(ad, out, n0=rows, n1=cols, ld=cols, nloops=2, keyed=True, out_dtype=H.F64))
     torch.cuda.synchronize()
-    assert nest.last_kernel() != "rowwise_tma_dsmem"
+    assert nest.last_kernel() == "rowwise_tma_dsmem"
     assert_rel(out.cpu().numpy(), oracle.rowsum_f32(a, rows, cols))
     off = gen.csr_offsets(300, 5000)
     v = gen.gen_f32(gen.SEED_C3, 0, 5000)
