@@ -257,7 +257,11 @@ typedef struct {
   int32_t keyed;         /* 0: one total (folded up to the node level);
                             1: one result per loop-0 iteration (row-wise / CSR)            */
   const void* in;        /* device; this rank's shard: flat [n0_local], dense rows
-                            [n0_local][ld], or CSR values                                  */
+                            [n0_local][ld], or CSR values.  Element-aligned is enough: a
+                            pointer off a 16-byte boundary (a tensor slice) keeps the fused
+                            kernels (enclosing-granule TMA copies; CSR: offsets + shift in
+                            a workspace copy), reading never past the granule of a valid
+                            element                                                        */
   int64_t n0;            /* GLOBAL extent of loop 0 (sharded over the GPU level)           */
   int64_t n1;            /* dense extent of loop 1 (0 for CSR)                              */
   int64_t ld;            /* dense row stride in elements (>= n1)                            */

@@ -204,8 +204,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
   auto cover_by = [&](int64_t p, int64_t who) {
     if constexpr (VERIFY) {
       if (a.verify & V_COVERAGE) {
-        a.owner[p] = who;
-        atomicAdd(&a.count[p], 1u);
+        a.owner[p - a.in_shift] = who;
+        atomicAdd(&a.count[p - a.in_shift], 1u);
       }
     }
   };
@@ -928,12 +928,39 @@ bool segmented_matches(const NestArgs& a, const char** why) {
   }
   if (a.radix[S_WARP] != WARPS) { *why = "W must be 8"; return false; }
   if (a.n1 >= 0x7FFFFFF0) { *why = "nnz per rank must be < 2^31 (32-bit window positions)"; return false; }
-  if (((uintptr_t)a.in & 15) != 0) { *why = "values not 16-byte aligned"; return false; }
+  if (((uintptr_t)a.in & 3) != 0) { *why = "values not element-aligned"; return false; }
   return true;
 }
 
-cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t nnz, cudaStream_t s, const char** name) {
+// offsets + shift into the workspace copy (misaligned values, below)
+__global__ void shift_offsets_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
+                                     int32_t shift) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] + shift;
+}
+
+cudaError_t launch_segmented(const NestArgs& a_call, void* wsbuf, int64_t nnz, int64_t* off_ws, cudaStream_t s,
+                             const char** name) {
   *name = "segmented_csr";
+  // values off a 16-byte boundary (a slice of a tensor): the kernel sees the
+  // array from the granule boundary before them — in_shift more elements —
+  // and reads offsets + in_shift from a workspace copy, so TMA windows and the
+  // tensor map stay aligned and the aligned call's kernel is untouched; the
+  // elements before the first row belong to no row; coverage is written at
+  // position - in_shift
+  NestArgs a = a_call;
+  a.in_shift = (int32_t)(((uintptr_t)a_call.in & 15) / 4);
+  if (a.in_shift) {
+    if (!off_ws) return cudaErrorInvalidValue;
+    a.in = (const float*)a_call.in - a.in_shift;
+    a.n1 = a_call.n1 + a.in_shift;
+    const int64_t n = a.n0 + 1;
+    const int grid = (int)((n + 255) / 256 < 4 * 148 ? (n + 255) / 256 : 4 * 148);
+    shift_offsets_kernel<<<grid, 256, 0, s>>>(a_call.offsets, off_ws, n, a.in_shift);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    a.offsets = off_ws;
+  }
   const int64_t maxseg = max_segments(nnz);
   unsigned char* p = (unsigned char*)wsbuf;
   SegWS ws;

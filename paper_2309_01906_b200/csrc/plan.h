@@ -59,7 +59,8 @@ struct NestArgs {
 
   // dynamic schedules (generic kernel: at most one level, on loop 0)
   int32_t dyn_level;        // nest level index or -1
-  int32_t pad0;
+  int32_t in_shift;         // segmented kernel: `in` moved back this many elements to a 16-byte
+                            // boundary; offsets are read + in_shift (0 otherwise)
   unsigned long long* dyn_tickets;
   int64_t dyn_slots;
 

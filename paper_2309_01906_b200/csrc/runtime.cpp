@@ -37,7 +37,8 @@ cudaError_t launch_hist(const NestArgs& a, int W, cudaStream_t s, const char** n
 int flat_resident_ctas_per_sm(int W);
 int flat_max_active_clusters(int K, int W);
 bool segmented_matches(const NestArgs& a, const char** why);
-cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t ws_nnz, cudaStream_t s, const char** name);
+cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t ws_nnz, int64_t* off_ws, cudaStream_t s,
+                             const char** name);
 size_t segmented_ws_bytes(int64_t nnz);
 void segmented_ws_qrow(int64_t nnz, size_t* off, size_t* len);
 cudaError_t launch_affine_rank_fold(const void* gathered, int G, void* out, cudaStream_t s);
@@ -293,6 +294,8 @@ struct hpar_nest {
   std::string last_kernel = "none";
   void* gather_buf = nullptr;  // node level of ordered ops: G gathered results
   void* seg_ws = nullptr;  // CSR segmented kernel workspace (grown on demand)
+  int64_t* seg_off_ws = nullptr;  // shifted offsets for values off a 16-byte boundary (grown on demand)
+  int64_t seg_off_rows = 0;
   size_t seg_ws_bytes = 0;
   int64_t seg_ws_nnz = -1;  // the nnz the workspace layout was built for (its capacity)
   float* halo_buf = nullptr;  // ghost exchange staging (grown on demand)
@@ -598,6 +601,7 @@ extern "C" hpar_status hpar_nest_destroy(hpar_nest_t n) {
     cudaFree(n->error_flag);
     cudaFree(n->barrier_word);
     cudaFree(n->seg_ws);
+    cudaFree(n->seg_off_ws);
     cudaFree(n->gather_buf);
     cudaFree(n->halo_buf);
   }
@@ -895,7 +899,15 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
       n->seg_ws_bytes = need;
       n->seg_ws_nnz = nnz;
     }
-    e = launch_segmented(A, n->seg_ws, n->seg_ws_nnz, stream, &name);
+    if (((uintptr_t)A.in & 15) && A.n0 + 1 > n->seg_off_rows) {
+      cudaFree(n->seg_off_ws);
+      n->seg_off_ws = nullptr;
+      n->seg_off_rows = 0;
+      cudaError_t ae = cudaMalloc(&n->seg_off_ws, (size_t)(A.n0 + 1) * 8);
+      if (ae != cudaSuccess) return fail(HPAR_E_NOMEM, "segmented offsets copy: %s", cudaGetErrorString(ae));
+      n->seg_off_rows = A.n0 + 1;
+    }
+    e = launch_segmented(A, n->seg_ws, n->seg_ws_nnz, n->seg_off_ws, stream, &name);
   } else if (teams_matches(A, &why)) {
     e = launch_teams(A, (int)n->W, stream, &name);
   } else if (collapsed) {

@@ -34,8 +34,9 @@ def env():
     return torch, H, nests
 
 
-def poisoned_input(torch, x: np.ndarray):
-    """x on the device with PAD poison elements before and after it"""
+def poisoned_input(torch, x: np.ndarray, shift: int = 0):
+    """x on the device with PAD (+ shift) poison elements before it and PAD
+    after it (shift > 0: x starts off a 16-byte boundary)"""
     if x.dtype == np.float32:
         poison = np.float32(np.nan)
     elif x.dtype == np.uint8:
@@ -44,10 +45,10 @@ def poisoned_input(torch, x: np.ndarray):
         poison = np.int64(0x5A5A5A5A5A5A5A5A)
     else:
         poison = np.int32(0x7FFFFF00)
-    buf = np.full(x.size + 2 * PAD, poison, dtype=x.dtype)
-    buf[PAD:PAD + x.size] = x
+    buf = np.full(x.size + 2 * PAD + shift, poison, dtype=x.dtype)
+    buf[PAD + shift:PAD + shift + x.size] = x
     d = torch.from_numpy(buf).cuda()
-    return d, d[PAD:PAD + x.size]
+    return d, d[PAD + shift:PAD + shift + x.size]
 
 
 class Canaried:
@@ -143,10 +144,10 @@ def test_segmented_bounds(env, oracle):
     off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     nnz = int(off[-1])
     v = gen.gen_f32(gen.SEED_C3, 0, nnz)
-    _, vd = poisoned_input(torch, v)
     offd = torch.from_numpy(off).cuda()  # offsets are not poisoned: a wild offset could hang the box
     nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=3)
-    for dt in (torch.float32, torch.float64):
+    for dt, shift in ((torch.float32, 0), (torch.float64, 0), (torch.float32, 1), (torch.float64, 3)):
+        _, vd = poisoned_input(torch, v, shift)  # shift: values 4 / 12 bytes off a granule
         out = Canaried(torch, (rows,), dt)
         owner = Canaried(torch, (nnz,), torch.int64, fill=-1)
         count = Canaried(torch, (nnz,), torch.int32)

@@ -505,6 +505,45 @@ def test_segmented_csr_kernel(H, torch_mod, oracle, case):
                 assert (ws_ == ws_[0]).all(), "a block's short rows span several warps"
 
 
+@pytest.mark.parametrize("mis", [4, 8, 12])
+@pytest.mark.parametrize("case", ["zipf", "one_huge_row", "edges", "unaligned_tail"])
+def test_segmented_misaligned_values(H, torch_mod, oracle, case, mis):
+    """CSR values 4, 8 or 12 bytes off a 16-byte boundary (a slice of a
+    larger tensor) stay on the fused kernel: it sees the array from the
+    granule boundary before them with every offset moved by the same shift.
+    Row sums vs the oracle, every nonzero visited exactly once (coverage
+    indexed by the caller's positions), over both output dtypes."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    off = dict(_csr_cases())[case]
+    rows, nnz = off.size - 1, int(off[-1])
+    v = gen.gen_f32(gen.SEED_C3, 0, nnz)
+    raw = torch.full((nnz + 16,), float("nan"), dtype=torch.float32, device="cuda")
+    e0 = mis // 4
+    xd = raw[e0:e0 + nnz]
+    xd.copy_(torch.from_numpy(v).cuda())
+    assert xd.data_ptr() % 16 == mis
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=5)
+    offd = torch.from_numpy(off).cuda()
+    owner = torch.full((nnz,), -1, dtype=torch.int64, device="cuda")
+    count = torch.zeros(nnz, dtype=torch.int32, device="cuda")
+    for dt, odt in ((torch.float64, H.F64), (torch.float32, H.F32)):
+        out = torch.full((rows,), -1.0, dtype=dt, device="cuda")
+        count.zero_()
+        d = H.make_desc(xd, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd, out_dtype=odt,
+                        verify=H.VERIFY_COVERAGE, owner=owner, count=count)
+        nest.parallel_for_reduce(d)
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "segmented_csr"
+        assert_rel(out.cpu().numpy().astype(np.float64), oracle.segsum_f32(v, off))
+        assert (count.cpu().numpy() == 1).all()
+        d = H.make_desc(xd, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd, out_dtype=odt)
+        out.fill_(-1.0)
+        nest.parallel_for_reduce(d)
+        torch.cuda.synchronize()
+        assert_rel(out.cpu().numpy().astype(np.float64), oracle.segsum_f32(v, off))
+
+
 def _probe_expect(oracle, level, C, K, W, rounds):
     """The oracle's fold for every task of the probe (hpar_barrier_probe):
     sum over rounds of the sum over the task's sibling group of
