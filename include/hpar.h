@@ -266,7 +266,9 @@ typedef struct {
   int64_t n1;            /* dense extent of loop 1 (0 for CSR)                              */
   int64_t ld;            /* dense row stride in elements (>= n1)                            */
   const int64_t* offsets;/* CSR: device int64 [n0_local + 1], local row offsets, or NULL  */
-  int64_t max_inner;     /* CSR: max row length (required with schedule NONE on loop 1)    */
+  int64_t max_inner;     /* CSR: max row length (required with schedule NONE on loop 1, and
+                            by the fused CSR kernel at >= 2^31 nonzeros per rank, where
+                            max_inner * 256 < 2^31 must hold; 0 = not given)                */
   void* out;             /* device.  keyed == 0: accumulator scalar (SUM i32/i64 -> int64,
                             f32/f64 -> double; MIN/MAX same types) or uint64[256] bins;
                             valid on EVERY rank after the stream completes (the node level

@@ -927,9 +927,61 @@ bool segmented_matches(const NestArgs& a, const char** why) {
     return false;
   }
   if (a.radix[S_WARP] != WARPS) { *why = "W must be 8"; return false; }
-  if (a.n1 >= 0x7FFFFFF0) { *why = "nnz per rank must be < 2^31 (32-bit window positions)"; return false; }
+  // positions inside a block of RB rows are 32-bit, relative to the block's
+  // window origin; the array itself is addressed in 64 bits (tensor-map
+  // coordinates in rows of 32 values: nnz < 2^36).  Below 2^31 nonzeros no
+  // block can overflow; above, the caller's row-length bound must prove it.
+  // (the launch checks the block spans at >= 2^31 nonzeros: segmented_span_ok)
+  if (a.n1 >= (1ll << 36) - 64) { *why = "nnz per rank must be < 2^36"; return false; }
   if (((uintptr_t)a.in & 3) != 0) { *why = "values not element-aligned"; return false; }
   return true;
+}
+
+// the largest span (nonzeros) of a block of RB rows
+__global__ void block_span_kernel(const int64_t* __restrict__ off, int64_t R, unsigned long long* span) {
+  const int64_t nb = (R + RB - 1) / RB;
+  unsigned long long m = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = (b + 1) * RB < R ? (b + 1) * RB : R;
+    const unsigned long long d = (unsigned long long)(off[e] - off[b * RB]);
+    m = d > m ? d : m;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+    m = v > m ? v : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(span, m);
+}
+
+// Positions inside a row block are 32-bit: below 2^31 nonzeros per rank no
+// block can overflow; above, either the caller's row-length bound proves it
+// (max_inner * RB < 2^31) or a check kernel measures the block spans, which
+// needs one host synchronisation (not possible while a graph is captured).
+// `scratch`: 8 device bytes.  Sets *ok; returns a CUDA error or success.
+cudaError_t segmented_span_ok(const NestArgs& a, unsigned long long* scratch, cudaStream_t s, bool* ok,
+                              bool* needs_sync) {
+  constexpr long long kLim = 0x7FFFFF00ll;
+  *needs_sync = false;
+  *ok = true;
+  if (a.n1 < 0x7FFFFFF0 || (a.max_inner > 0 && a.max_inner * RB < kLim)) return cudaSuccess;
+  *needs_sync = true;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(s, &cs);
+  if (e != cudaSuccess) return e;
+  if (cs != cudaStreamCaptureStatusNone) {
+    *ok = false;
+    return cudaSuccess;
+  }
+  unsigned long long h = 0;
+  if ((e = cudaMemsetAsync(scratch, 0, 8, s)) != cudaSuccess) return e;
+  const int64_t nb = (a.n0 + RB - 1) / RB;
+  const int grid = (int)((nb + 255) / 256 < 4 * 148 ? (nb + 255) / 256 : 4 * 148);
+  if (grid > 0) block_span_kernel<<<grid, 256, 0, s>>>(a.offsets, a.n0, scratch);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(&h, scratch, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  *ok = (long long)h < kLim;
+  return cudaSuccess;
 }
 
 // offsets + shift into the workspace copy (misaligned values, below)

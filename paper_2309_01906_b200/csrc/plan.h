@@ -77,6 +77,8 @@ struct NestArgs {
   void* node_win;         // ncclWindow_t of the slot buffer
   int32_t node_parity;    // which half of the slot buffer this call uses
   int32_t node_slot;      // bytes per rank slot
+
+  int64_t max_inner;      // CSR: the caller's bound on a row's length (0 = not given)
 };
 
 }  // namespace hpar

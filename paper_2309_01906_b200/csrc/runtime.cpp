@@ -39,6 +39,8 @@ int flat_max_active_clusters(int K, int W);
 bool segmented_matches(const NestArgs& a, const char** why);
 cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t ws_nnz, int64_t* off_ws, cudaStream_t s,
                              const char** name);
+cudaError_t segmented_span_ok(const NestArgs& a, unsigned long long* scratch, cudaStream_t s, bool* ok,
+                              bool* needs_sync);
 size_t segmented_ws_bytes(int64_t nnz);
 void segmented_ws_qrow(int64_t nnz, size_t* off, size_t* len);
 cudaError_t launch_affine_rank_fold(const void* gathered, int G, void* out, cudaStream_t s);
@@ -797,6 +799,7 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   A.grid_ticket = n->grid_ticket;
   A.cluster_partials = n->cluster_partials;
   A.error_flag = n->error_flag;
+  A.max_inner = d->max_inner;
   A.dyn_tickets = n->dyn_tickets;
   A.dyn_slots = n->dyn_slots;
   A.dyn_level = -1;
@@ -884,6 +887,16 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
     // fewer nonzeros keeps the same offsets, so the self-reset tickets and the
     // all-ones empty queue slots stay where the kernel looks for them.
     const int64_t nnz = d->n1;
+    {
+      bool span_ok = true, synced = false;
+      // (error_flag's 64 device bytes serve as the check's scratch word)
+      CUDA_TRY(segmented_span_ok(A, (unsigned long long*)n->error_flag, stream, &span_ok, &synced));
+      if (!span_ok)
+        return fail(HPAR_E_UNSUPPORTED,
+                    synced ? "segmented CSR: a block of 256 rows spans >= 2^31 nonzeros (32-bit positions)"
+                           : "segmented CSR: >= 2^31 nonzeros per rank while capturing a graph: the block-span "
+                             "check needs a host sync; pass desc->max_inner with max_inner * 256 < 2^31");
+    }
     if (nnz > n->seg_ws_nnz) {
       const size_t need = segmented_ws_bytes(nnz);
       cudaFree(n->seg_ws);

@@ -11,7 +11,8 @@ times (same nests, geometry and kernels):
   c6  16384^2 + ghost ring at the 128-byte pitch: two sweeps bit-exact vs
       the oracle's numpy steps over the whole array
 Edge cases at their stated sizes: C4 with 2^32 equal bytes (bin 0 = 2^32,
-beyond any u32 counter), C3 with one row of 2^26 nonzeros between empty rows.
+beyond any u32 counter), C3 with one row of 2^26 nonzeros between empty rows,
+C3 past 2^31 nonzeros per rank (sampled rows around position 2^31).
 The oracle runs range by range in a process pool (tests/fullsize_oracle.py:
 every quantity is exact and additive over disjoint ranges).
 Inputs come from the device generator, which is cross-checked bit for bit
@@ -258,3 +259,41 @@ def test_c3_single_huge_row(env, oracle):
     exact = oracle.sum_u64(gen.gen_f32_k(gen.SEED_C3, 0, nnz)) * 2.0 ** -24
     assert got[0] == 0 and got[2] == 0 and got[3] == 0
     assert_rel(got[1:2], np.array([exact]))
+
+
+def test_c3_beyond_2e31_nonzeros(env, oracle):
+    """C3 past 32-bit sizes (the 180 GB HBM budget allows ~4e10 fp32
+    nonzeros per GPU): 2^23 zipf rows (the longest 1.8e7 nonzeros) over
+    2^31 + 49383 nonzeros.  Positions inside a 256-row block stay 32-bit;
+    the launch proves every block spans < 2^31 (the block-span check, no
+    max_inner given).  Sampled rows — those around positions 2^31 and 2^32 /
+    the array end, the longest, random ones — vs the oracle's segment sums;
+    the sum of all rows vs the oracle's exact total."""
+    torch, H, nests, L = env
+    from tests import fullsize_oracle as F
+    rows, nnz = 1 << 23, (1 << 31) + 4 * 12345 + 3
+    off = gen.csr_offsets(rows, nnz)
+    assert int(off[-1]) == nnz
+    lens = np.diff(off)
+    x = torch.empty(nnz, dtype=torch.float32, device="cuda")
+    L.hpar_inputs_fill_f32(gen.SEED_C3, 0, nnz, x.data_ptr(), None)
+    offd = torch.from_numpy(off).cuda()
+    out = torch.full((rows,), -1.0, dtype=torch.float64, device="cuda")
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8)
+    d = H.make_desc(x, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd, out_dtype=H.F64)
+    for _ in range(2):
+        out.fill_(-1.0)
+        nest.parallel_for_reduce(d)
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "segmented_csr"
+    got = out.cpu().numpy()
+    r31 = int(np.searchsorted(off, 1 << 31, side="right")) - 1  # the row holding position 2^31
+    rng = np.random.default_rng(5)
+    sample = set(range(max(0, r31 - 300), min(rows, r31 + 300))) | set(range(rows - 300, rows))
+    sample |= set(np.argsort(lens)[-8:].tolist()) | set(rng.integers(0, rows, 500).tolist())
+    for r in sorted(sample):
+        b, n = int(off[r]), int(lens[r])
+        want = oracle.segsum_f32(gen.gen_f32(gen.SEED_C3, b, n), np.array([0, n], dtype=np.int64))
+        assert_rel(got[r:r + 1], want)
+    exact = F.exact_numerator_sum(gen.SEED_C3, nnz) * 2.0 ** -24
+    assert abs(got.sum() - exact) <= 1e-9 * exact
