@@ -127,6 +127,40 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
               }
             }
           }
+        } else if constexpr (sizeof(In) == 8) {
+          // 8-byte elements: a lane's 4 elements are 32 bytes, two aligned
+          // LDS.128 (three when the input sits 8 bytes off a granule)
+          using V = typename std::conditional<std::is_floating_point<In>::value, double2, longlong2>::type;
+          const V* g = (const V*)(dsm + (size_t)s * stride);
+#pragma unroll 2
+          for (int f = warp * 32 + lane; f < vec_per_tile; f += W * 32) {
+            V lo, hi;
+            if constexpr (MIS) {
+              const V a0 = g[2 * f], a1 = g[2 * f + 1], a2 = g[2 * f + 2];
+              lo.x = a0.y; lo.y = a1.x; hi.x = a1.y; hi.y = a2.x;
+            } else {
+              lo = g[2 * f];
+              hi = g[2 * f + 1];
+            }
+            if constexpr (OP == OP_SUM) {
+              acc += (lo.x + lo.y) + (hi.x + hi.y);  // integers: two's complement, wraps mod 2^64
+            } else {
+              acc = OpT<OP, Acc>::combine(acc, (Acc)lo.x);
+              acc = OpT<OP, Acc>::combine(acc, (Acc)lo.y);
+              acc = OpT<OP, Acc>::combine(acc, (Acc)hi.x);
+              acc = OpT<OP, Acc>::combine(acc, (Acc)hi.y);
+            }
+            if constexpr (VERIFY) {
+              for (int q = 0; q < 4; ++q) {
+                const int64_t it = base + 4 * f + q;
+                if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
+                if (a.verify & V_FINGERPRINT) {
+                  const uint64_t g2 = a.global_begin + (uint64_t)it;
+                  fpo += fp_mix(g2); fpw += fp_mix2(g2, (uint64_t)leaf); fpn += 1;
+                }
+              }
+            }
+          }
         } else if constexpr (sizeof(In) == 4) {
 #pragma unroll 4
           for (int f = warp * 32 + lane; f < vec_per_tile; f += W * 32) {
@@ -228,8 +262,12 @@ cudaError_t launch_v(const NestArgs& a, int W, int tile, cudaStream_t s) {
 bool flat_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 1 || a.keyed) { *why = "not a flat total"; return false; }
   if (a.op == OP_HIST || a.op == OP_AFFINE) { *why = "sum/min/max only"; return false; }
-  if (a.in_dtype != DT_F32 && a.in_dtype != DT_I32) { *why = "dtype"; return false; }
-  if (((uintptr_t)a.in & 3) != 0) { *why = "input not element-aligned"; return false; }
+  if (a.in_dtype != DT_F32 && a.in_dtype != DT_I32 && a.in_dtype != DT_F64 && a.in_dtype != DT_I64) {
+    *why = "dtype";
+    return false;
+  }
+  const int64_t esz = (a.in_dtype == DT_F64 || a.in_dtype == DT_I64) ? 8 : 4;
+  if (((uintptr_t)a.in & (esz - 1)) != 0) { *why = "input not element-aligned"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
   LevelView v = device_levels(a);
   if (v.n != 4) { *why = "needs cluster, CTA, warp, lane levels"; return false; }
@@ -242,7 +280,7 @@ bool flat_matches(const NestArgs& a, const char** why) {
   const int64_t tile = k->chunk;
   if (l->sched != SCHED_STATIC_CHUNK || l->chunk != 4) { *why = "lane must be static(4)"; return false; }
   if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 128) { *why = "warp must be static(128)"; return false; }
-  if (k->sched != SCHED_STATIC_CHUNK || tile % (128 * W) != 0 || tile * 4 > 32768) {
+  if (k->sched != SCHED_STATIC_CHUNK || tile % (128 * W) != 0 || tile * esz > 32768) {
     *why = "CTA must be static(tile), tile a multiple of 128*W, <= 32 KiB";
     return false;
   }
@@ -259,6 +297,14 @@ cudaError_t launch_flat(const NestArgs& a, int W, cudaStream_t s, const char** n
     if (a.op == OP_SUM) return launch_v<float, double, OP_SUM>(a, W, tile, s);
     if (a.op == OP_MIN) return launch_v<float, double, OP_MIN>(a, W, tile, s);
     if (a.op == OP_MAX) return launch_v<float, double, OP_MAX>(a, W, tile, s);
+  } else if (a.in_dtype == DT_F64) {
+    if (a.op == OP_SUM) return launch_v<double, double, OP_SUM>(a, W, tile, s);
+    if (a.op == OP_MIN) return launch_v<double, double, OP_MIN>(a, W, tile, s);
+    if (a.op == OP_MAX) return launch_v<double, double, OP_MAX>(a, W, tile, s);
+  } else if (a.in_dtype == DT_I64) {
+    if (a.op == OP_SUM) return launch_v<long long, long long, OP_SUM>(a, W, tile, s);
+    if (a.op == OP_MIN) return launch_v<long long, long long, OP_MIN>(a, W, tile, s);
+    if (a.op == OP_MAX) return launch_v<long long, long long, OP_MAX>(a, W, tile, s);
   } else {
     if (a.op == OP_SUM) return launch_v<int32_t, long long, OP_SUM>(a, W, tile, s);
     if (a.op == OP_MIN) return launch_v<int32_t, long long, OP_MIN>(a, W, tile, s);

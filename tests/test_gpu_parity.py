@@ -364,6 +364,30 @@ def test_rowwise_ragged_rows(H, torch_mod, oracle, n0, n1, ld, mis):
         compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, C=C, K=K, W=W)
 
 
+@pytest.mark.parametrize("mis", [0, 8])
+@pytest.mark.parametrize("dt", ["f64", "i64"])
+def test_flat_8byte_elements(H, torch_mod, oracle, dt, mis):
+    """fp64 and int64 inputs (SURVEY §8(b) dtypes) on the fused flat kernel:
+    a lane's four elements are 32 bytes (two aligned vectors, three when the
+    input sits 8 bytes off a granule).  SUM / MIN / MAX results, owner map
+    and every level's partials vs the oracle; int64 sums of values near 2^62
+    wrap mod 2^64 exactly as the oracle's."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c5_nest(K=2)
+    C, K, W = 5, 2, 8
+    rng = np.random.default_rng(64)
+    for n in (1, 3, 4096 * 2 * 5, 4096 * 2 * 7 + 4 * 99 + 3, 300001):
+        if dt == "f64":
+            x = rng.standard_normal(n) * 1e3
+        else:
+            x = rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)
+        for op in (H.OP_SUM, H.OP_MIN, H.OP_MAX):
+            res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis)
+            assert res["kernel"] == "flat_tma"
+            compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
+
+
 def test_rowwise_fused_kernel_small(H, torch_mod, oracle):
     """The fused row-wise kernel (config-2 nest) on 50 x 4096 and ragged
     columns: rows, owner map, per-row lane/warp/CTA partials vs oracle."""
