@@ -7,7 +7,9 @@
 //     warp     static(128)   loop 1
 //     lane     static(4)     loop 1
 // One result per row (keyed by loop 0): the row owner is the cluster, whose
-// CTAs, warps and lanes combine every row.
+// CTAs, warps and lanes combine every row.  SUM / MIN / MAX over
+// fp32 (the config-2 case, fp32 lane/warp tree), fp64, int32 and int64
+// (64-bit partials, 8-byte DSMEM slots).
 //
 // B200 design (per cluster, per row):
 //   * each CTA's producer warp streams its n1/K-column segment of the row
@@ -32,6 +34,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <type_traits>
 #include "fused_common.cuh"
 
 namespace hpar {
@@ -42,35 +45,101 @@ constexpr int kSlots = 16;      // DSMEM row-slot ring depth in the leader
 constexpr int kMaxPush = 32;    // K*W <= 32 warp partials per row
 
 
-// NV: float4 vectors per lane per row (qcols == 128*W*NV); 0 = generic loop;
-// -1 = ragged rows: any n1, ld and 4-byte aligned input.  Then the CTAs'
-// column blocks follow the static partition (the first n1 % K CTAs take one
-// column more), a CTA's segment of a row may start anywhere in a 16-byte
-// granule, so the producer copies the enclosing granules and the lanes shift
-// (shift4) by the row's offset; qcols is the ring-stage stride in floats.
+// NV (fp32 sums): float4 vectors per lane per row (qcols == 128*W*NV);
+// 0 = generic loop; -1 = ragged rows: any n1, ld and element-aligned input.
+// Then the CTAs' column blocks follow the static partition (the first
+// n1 % K CTAs take one column more), a CTA's segment of a row may start
+// anywhere in a 16-byte granule, so the producer copies the enclosing
+// granules and the lanes shift by the row's offset (load_quad).
 bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int elem_bytes(const NestArgs& a) { return (a.in_dtype == DT_F64 || a.in_dtype == DT_I64) ? 8 : 4; }
 
 // rows the aligned path cannot copy whole: n1 not a multiple of 4K, or rows
 // (ld, the base pointer) off 16-byte boundaries
 bool rowwise_ragged(const NestArgs& a) {
-  return a.n1 % (4 * a.K) != 0 || a.ld % 4 != 0 || ((uintptr_t)a.in & 15) != 0;
+  const int64_t esz = elem_bytes(a);
+  return a.n1 % (4 * a.K) != 0 || (a.ld * esz) % 16 != 0 || ((uintptr_t)a.in & 15) != 0;
 }
 
-// ring-stage stride in floats: the aligned path's n1/K; a ragged segment of up
-// to ceil(n1/K) columns starting anywhere in a granule needs one granule more
-int rowwise_stride(const NestArgs& a) {
-  if (!rowwise_ragged(a)) return (int)(a.n1 / a.K);
+// ring-stage stride in bytes: the aligned path's n1/K columns; a ragged
+// segment of up to ceil(n1/K) columns starting anywhere in a granule needs
+// one granule more
+int64_t rowwise_stage_bytes(const NestArgs& a) {
+  const int64_t esz = elem_bytes(a);
+  if (!rowwise_ragged(a)) return a.n1 / a.K * esz;
   const int64_t qmax = (a.n1 + a.K - 1) / a.K;
-  return (int)(((qmax + 3) / 4 + 1) * 4);
+  return ((qmax * esz + 15) / 16 + 1) * 16;
 }
 
-template <bool VERIFY, int NV>
+// Element and partial types.  In: the input element; P: the lane / warp
+// partial and the DSMEM slot (fp32 for fp32 sums — the fp32 tree of reading
+// #4 — else the 64-bit accumulator); X: the combiner's and the exported
+// partials' type (fp64 for floating point, int64 for integers).
+template <typename In> struct RwX { using T = long long; };
+template <> struct RwX<float> { using T = double; };
+template <> struct RwX<double> { using T = double; };
+template <typename In, int OP>
+using RwP = typename std::conditional<std::is_same<In, float>::value && OP == OP_SUM, float,
+                                      typename RwX<In>::T>::type;
+
+// the four elements of lane vector f (elements 4f .. 4f+3 of the CTA's
+// block), from a ring stage whose data start `mis` bytes into its first
+// 16-byte granule (0 unless ragged)
+template <typename In, bool RAG>
+__device__ __forceinline__ void load_quad(const unsigned char* stage, int f, uint32_t mis, In (&e)[4]) {
+  if constexpr (sizeof(In) == 4) {
+    using V = typename std::conditional<std::is_floating_point<In>::value, float4, int4>::type;
+    const V* g = (const V*)stage;
+    V t = g[f];
+    if (RAG && mis) t = shift4(t, g[f + 1], mis >> 2);
+    e[0] = t.x; e[1] = t.y; e[2] = t.z; e[3] = t.w;
+  } else {
+    using V = typename std::conditional<std::is_floating_point<In>::value, double2, longlong2>::type;
+    const V* g = (const V*)stage;
+    if (RAG && mis) {
+      const V a0 = g[2 * f], a1 = g[2 * f + 1], a2 = g[2 * f + 2];
+      e[0] = a0.y; e[1] = a1.x; e[2] = a1.y; e[3] = a2.x;
+    } else {
+      const V lo = g[2 * f], hi = g[2 * f + 1];
+      e[0] = lo.x; e[1] = lo.y; e[2] = hi.x; e[3] = hi.y;
+    }
+  }
+}
+
+__device__ __forceinline__ void st_async_part(uint32_t addr, uint32_t bar, float v) {
+  st_async_u32(addr, bar, __float_as_uint(v));
+}
+__device__ __forceinline__ void st_async_part(uint32_t addr, uint32_t bar, double v) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr),
+               "l"(__double_as_longlong(v)), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_part(uint32_t addr, uint32_t bar, long long v) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr), "l"(v),
+               "r"(bar)
+               : "memory");
+}
+
+template <typename X>
+__device__ __forceinline__ void store_row(const NestArgs& a, int64_t row, X v) {
+  switch (a.out_dtype) {
+    case DT_F32: ((float*)a.out)[row] = (float)v; break;
+    case DT_F64: ((double*)a.out)[row] = (double)v; break;
+    default: ((long long*)a.out)[row] = (long long)v; break;
+  }
+}
+
+template <typename In, int OP, bool VERIFY, int NV>
 __global__ void __launch_bounds__(1024, 1)
-    rowwise_kernel(const __grid_constant__ NestArgs a, int W, int qcols, int kStages) {
+    rowwise_kernel(const __grid_constant__ NestArgs a, int W, int qcols, int kStages, int stage_bytes) {
+  using P = RwP<In, OP>;
+  using X = typename RwX<In>::T;
+  constexpr bool F32SUM = std::is_same<P, float>::value;
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ __align__(8) uint64_t row_full[kSlots], slot_empty[kSlots];
-  __shared__ __align__(8) float slot[kSlots][kMaxPush];
+  __shared__ __align__(8) P slot[kSlots][kMaxPush];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K;
@@ -83,8 +152,8 @@ __global__ void __launch_bounds__(1024, 1)
   const int64_t q1 = a.n1 / K, r1 = a.n1 % K;
   const int64_t col0 = NV < 0 ? (int64_t)crank * q1 + ((int64_t)crank < r1 ? crank : r1) : (int64_t)crank * qcols;
   const int lenk = NV < 0 ? (int)(q1 + ((int64_t)crank < r1 ? 1 : 0)) : qcols;  // this CTA's columns
-  const float* x = (const float*)a.in;
-  const uint32_t seg_bytes = (uint32_t)qcols * 4;
+  const In* x = (const In*)a.in;
+  const uint32_t seg_bytes = (uint32_t)stage_bytes;
   const int npush = K * W;
 
   if (threadIdx.x == 0) {
@@ -104,7 +173,7 @@ __global__ void __launch_bounds__(1024, 1)
     // ------------------------------ producer warp: TMA row segments ----
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      const float* src = x + row0 * a.ld + col0;
+      const In* src = x + row0 * a.ld + col0;
       int s = 0;
       uint32_t ph = 0;
       for (uint32_t j = 0; j < nrows; ++j) {
@@ -113,7 +182,7 @@ __global__ void __launch_bounds__(1024, 1)
           // the granules enclosing this row's segment (never past the
           // granule of a valid element)
           const uint32_t mis = (uint32_t)((uintptr_t)src & 15);
-          const uint32_t bytes = lenk ? (uint32_t)((lenk * 4 + mis + 15) & ~15u) : 0u;
+          const uint32_t bytes = lenk ? (uint32_t)((lenk * (uint32_t)sizeof(In) + mis + 15) & ~15u) : 0u;
           mbar_arrive_expect_tx(&full[s], bytes);
           if (bytes) bulk_g2s(dsm + (size_t)s * seg_bytes, (const unsigned char*)src - mis, bytes, &full[s], pol);
         } else {
@@ -134,23 +203,19 @@ __global__ void __launch_bounds__(1024, 1)
         const uint32_t j = j0 + g;
         const bool live = j < nrows;
         const int s = (int)(j % kSlots);
-        double v = 0.0;
+        X v = OpT<OP, X>::identity();
         if (live) {
-          if (e == 0) mbar_arrive_expect_tx(&row_full[s], (uint32_t)(npush * 4));
+          if (e == 0) mbar_arrive_expect_tx(&row_full[s], (uint32_t)(npush * sizeof(P)));
           mbar_wait_cluster(&row_full[s], (j / kSlots) & 1);
-          v = (double)slot[s][e];
+          v = (X)slot[s][e];
         }
         // warp partials -> CTA partials (every W lanes), ordered
-        for (int off = 1; off < W; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        for (int off = 1; off < W; off <<= 1) v = OpT<OP, X>::combine(v, __shfl_xor_sync(0xffffffffu, v, off));
         if (VERIFY && live && (a.verify & V_PARTIALS) && (e % W) == 0)
-          export_slot<double>(a, S_CTA, (row0 + j) * K + e / W, v);
+          export_slot<X>(a, S_CTA, (row0 + j) * K + e / W, v);
         // CTA partials -> row (cluster), ordered
-        for (int off = W; off < npush; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (live && e == 0) {
-          const int64_t row = row0 + j;
-          if (a.out_dtype == DT_F32) ((float*)a.out)[row] = (float)v;
-          else ((double*)a.out)[row] = v;
-        }
+        for (int off = W; off < npush; off <<= 1) v = OpT<OP, X>::combine(v, __shfl_xor_sync(0xffffffffu, v, off));
+        if (live && e == 0) store_row<X>(a, row0 + j, v);
         // free the slot in every CTA of the cluster (relaxed: it orders only
         // the slot reads above, which the shuffles have consumed)
         if (live && e < K) mbar_arrive_cluster_relaxed(mapa(smem_addr(&slot_empty[s]), (uint32_t)e));
@@ -167,31 +232,35 @@ __global__ void __launch_bounds__(1024, 1)
     uint32_t ph = 0, sph = 0;
     for (uint32_t j = 0; j < nrows; ++j) {
       mbar_wait(&full[s], ph);
-      const float4* st = (const float4*)(dsm + (size_t)s * seg_bytes);
-      float acc = 0.f;
-      if constexpr (NV > 0) {
+      const unsigned char* stage = dsm + (size_t)s * seg_bytes;
+      P acc = OpT<OP, P>::identity();
+      if constexpr (NV > 0 && F32SUM) {
+        const float4* st = (const float4*)stage;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const float4 t = st[(v * W + warp) * 32 + lane];
           acc += (t.x + t.y) + (t.z + t.w);
         }
-      } else if constexpr (NV < 0) {
-        const uint32_t m4 = (uint32_t)((((uintptr_t)(x + (row0 + j) * a.ld + col0)) & 15) >> 2);
-        for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
-          float4 t = st[f];
-          if (m4) t = shift4(t, st[f + 1], m4);
-          const int rem = lenk - 4 * f;  // the last vector may be partial: zeros keep the tree's order
-          if (rem < 4) {
-            t.w = 0.f;
-            if (rem < 3) t.z = 0.f;
-            if (rem < 2) t.y = 0.f;
-          }
-          acc += (t.x + t.y) + (t.z + t.w);
-        }
       } else {
+        const uint32_t mis = NV < 0 ? (uint32_t)(((uintptr_t)(x + (row0 + j) * a.ld + col0)) & 15) : 0u;
         for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
-          const float4 t = st[f];
-          acc += (t.x + t.y) + (t.z + t.w);
+          In e[4];
+          load_quad<In, (NV < 0)>(stage, f, mis, e);
+          P t[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) t[k] = (P)e[k];
+          if constexpr (NV < 0) {
+            const int rem = lenk - 4 * f;  // the last vector may be partial: identities keep the tree's order
+#pragma unroll
+            for (int k = 1; k < 4; ++k)
+              if (rem <= k) t[k] = OpT<OP, P>::identity();
+          }
+          if constexpr (OP == OP_SUM) {
+            acc += (t[0] + t[1]) + (t[2] + t[3]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc = OpT<OP, P>::combine(acc, t[k]);
+          }
         }
       }
       if constexpr (VERIFY) {
@@ -206,17 +275,17 @@ __global__ void __launch_bounds__(1024, 1)
       if (++s == kStages) { s = 0; ph ^= 1; }
       if constexpr (VERIFY) {
         if (a.verify & V_PARTIALS)
-          export_slot<double>(a, S_LANE_IN, (row0 + j) * (int64_t)(npush * 32) + push_idx * 32 + lane, acc);
+          export_slot<X>(a, S_LANE_IN, (row0 + j) * (int64_t)(npush * 32) + push_idx * 32 + lane, (X)acc);
       }
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      for (int off = 1; off < 32; off <<= 1) acc = OpT<OP, P>::combine(acc, __shfl_xor_sync(0xffffffffu, acc, off));
       if (lane == 0) {
         if constexpr (VERIFY) {
-          if (a.verify & V_PARTIALS) export_slot<double>(a, S_WARP, (row0 + j) * npush + push_idx, acc);
+          if (a.verify & V_PARTIALS) export_slot<X>(a, S_WARP, (row0 + j) * npush + push_idx, (X)acc);
         }
         if (j >= (uint32_t)kSlots) mbar_wait_relaxed_cluster(&slot_empty[ss], sph ^ 1);
-        st_async_u32(leader_slot_base + (uint32_t)((ss * kMaxPush + push_idx) * 4),
-                     leader_full_base + (uint32_t)(ss * 8), __float_as_uint(acc));
+        st_async_part(leader_slot_base + (uint32_t)((ss * kMaxPush + push_idx) * sizeof(P)),
+                      leader_full_base + (uint32_t)(ss * 8), acc);
       }
       if (++ss == kSlots) { ss = 0; sph ^= 1; }
     }
@@ -228,10 +297,10 @@ __global__ void __launch_bounds__(1024, 1)
   cluster_sync_all();
 }
 
-template <bool V, int NV>
-cudaError_t launch_t(const NestArgs& a, int W, int qcols, int stages, cudaStream_t s) {
-  auto kern = rowwise_kernel<V, NV>;
-  const size_t smem = (size_t)stages * qcols * 4;
+template <typename In, int OP, bool V, int NV>
+cudaError_t launch_t(const NestArgs& a, int W, int qcols, int stages, int stage_bytes, cudaStream_t s) {
+  auto kern = rowwise_kernel<In, OP, V, NV>;
+  const size_t smem = (size_t)stages * stage_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -246,24 +315,40 @@ cudaError_t launch_t(const NestArgs& a, int W, int qcols, int stages, cudaStream
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, W, qcols, stages);
+  return cudaLaunchKernelEx(&cfg, kern, a, W, qcols, stages, stage_bytes);
 }
 
-template <bool V>
-cudaError_t launch_nv(const NestArgs& a, int W, int qcols, int stages, cudaStream_t s) {
-  if (rowwise_ragged(a)) return launch_t<V, -1>(a, W, qcols, stages, s);
-  const int nv = (qcols % (128 * W) == 0) ? qcols / (128 * W) : 0;
-  switch (nv) {
-    case 1: return launch_t<V, 1>(a, W, qcols, stages, s);
-    case 2: return launch_t<V, 2>(a, W, qcols, stages, s);
-    case 4: return launch_t<V, 4>(a, W, qcols, stages, s);
-    case 8: return launch_t<V, 8>(a, W, qcols, stages, s);
-    default: return launch_t<V, 0>(a, W, qcols, stages, s);
+template <typename In, int OP, bool V>
+cudaError_t launch_nv(const NestArgs& a, int W, int qcols, int stages, int stage_bytes, cudaStream_t s) {
+  if (rowwise_ragged(a)) return launch_t<In, OP, V, -1>(a, W, qcols, stages, stage_bytes, s);
+  if constexpr (std::is_same<In, float>::value && OP == OP_SUM) {
+    const int nv = (qcols % (128 * W) == 0) ? qcols / (128 * W) : 0;
+    switch (nv) {
+      case 1: return launch_t<In, OP, V, 1>(a, W, qcols, stages, stage_bytes, s);
+      case 2: return launch_t<In, OP, V, 2>(a, W, qcols, stages, stage_bytes, s);
+      case 4: return launch_t<In, OP, V, 4>(a, W, qcols, stages, stage_bytes, s);
+      case 8: return launch_t<In, OP, V, 8>(a, W, qcols, stages, stage_bytes, s);
+      default: break;
+    }
+  }
+  return launch_t<In, OP, V, 0>(a, W, qcols, stages, stage_bytes, s);
+}
+
+template <typename In>
+cudaError_t launch_op(const NestArgs& a, int W, int qcols, int stages, int stage_bytes, cudaStream_t s) {
+  const bool v = a.verify != 0;
+  switch (a.op) {
+    case OP_SUM: return v ? launch_nv<In, OP_SUM, true>(a, W, qcols, stages, stage_bytes, s)
+                          : launch_nv<In, OP_SUM, false>(a, W, qcols, stages, stage_bytes, s);
+    case OP_MIN: return v ? launch_nv<In, OP_MIN, true>(a, W, qcols, stages, stage_bytes, s)
+                          : launch_nv<In, OP_MIN, false>(a, W, qcols, stages, stage_bytes, s);
+    case OP_MAX: return v ? launch_nv<In, OP_MAX, true>(a, W, qcols, stages, stage_bytes, s)
+                          : launch_nv<In, OP_MAX, false>(a, W, qcols, stages, stage_bytes, s);
+    default: return cudaErrorInvalidValue;
   }
 }
 
-
-int rowwise_stages(int qcols) {
+int rowwise_stages(int stage_bytes) {
   static int env = -2;
   if (env == -2) {
     const char* e = getenv("HPAR_RW_STAGES");
@@ -271,10 +356,10 @@ int rowwise_stages(int qcols) {
   }
   // default: ~16 KiB of row segments in flight per CTA; many small CTAs keep
   // more bytes in flight per SM than few deep ones (measured)
-  int st = (env >= 2 && env <= kMaxStages) ? env : (int)(16384 / ((size_t)qcols * 4));
+  int st = (env >= 2 && env <= kMaxStages) ? env : (int)(16384 / (size_t)stage_bytes);
   if (st < 2) st = 2;
   if (st > kMaxStages) st = kMaxStages;
-  while (st > 2 && (size_t)st * qcols * 4 > 200 * 1024) --st;
+  while (st > 2 && (size_t)st * stage_bytes > 200 * 1024) --st;
   return st;
 }
 
@@ -282,7 +367,11 @@ int rowwise_stages(int qcols) {
 
 bool rowwise_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 2 || !a.keyed || a.offsets) { *why = "not a dense keyed 2-loop nest"; return false; }
-  if (a.op != OP_SUM || a.in_dtype != DT_F32) { *why = "rowwise kernel: f32 sum only"; return false; }
+  if (a.op != OP_SUM && a.op != OP_MIN && a.op != OP_MAX) { *why = "rowwise kernel: sum / min / max"; return false; }
+  if (a.in_dtype != DT_F32 && a.in_dtype != DT_F64 && a.in_dtype != DT_I32 && a.in_dtype != DT_I64) {
+    *why = "rowwise kernel: dtype";
+    return false;
+  }
   if (a.verify & V_FINGERPRINT) { *why = "fingerprints not produced by the rowwise kernel"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
   LevelView v = device_levels(a);
@@ -298,17 +387,24 @@ bool rowwise_matches(const NestArgs& a, const char** why) {
   if (l->loop != 1 || l->sched != SCHED_STATIC_CHUNK || l->chunk != 4) { *why = "lane static(4)"; return false; }
   const int64_t K = a.K, W = a.radix[S_WARP];
   if (!pow2(K) || !pow2(W) || K * W > kMaxPush || W > 30) { *why = "K, W powers of two, K*W <= 32"; return false; }
-  if (((uintptr_t)a.in & 3) || a.ld < a.n1) { *why = "input not element-aligned or ld < n1"; return false; }
-  if ((int64_t)rowwise_stride(a) * 4 * 2 > 200 * 1024) { *why = "row segment too large for the smem ring"; return false; }
+  if (((uintptr_t)a.in & (elem_bytes(a) - 1)) || a.ld < a.n1) { *why = "input not element-aligned or ld < n1"; return false; }
+  if (rowwise_stage_bytes(a) * 2 > 200 * 1024) { *why = "row segment too large for the smem ring"; return false; }
   if (a.n1 == 0) { *why = "empty rows"; return false; }
   return true;
 }
 
 cudaError_t launch_rowwise(const NestArgs& a, int W, cudaStream_t s, const char** name) {
   *name = "rowwise_tma_dsmem";
-  const int qcols = rowwise_stride(a);
-  const int st = rowwise_stages(qcols);
-  return a.verify ? launch_nv<true>(a, W, qcols, st, s) : launch_nv<false>(a, W, qcols, st, s);
+  const int qcols = (int)(a.n1 / a.K);  // the aligned path's columns per CTA
+  const int sb = (int)rowwise_stage_bytes(a);
+  const int st = rowwise_stages(sb);
+  switch (a.in_dtype) {
+    case DT_F32: return launch_op<float>(a, W, qcols, st, sb, s);
+    case DT_F64: return launch_op<double>(a, W, qcols, st, sb, s);
+    case DT_I32: return launch_op<int32_t>(a, W, qcols, st, sb, s);
+    case DT_I64: return launch_op<long long>(a, W, qcols, st, sb, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace hpar

@@ -69,9 +69,9 @@ def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, 
     else:
         n_iter = n0 * (n1 if nloops == 2 else 1)
     xd = torch.from_numpy(x).cuda()
-    if ld and ld != n1:  # rows at stride ld; the padding columns hold NaN (a read of them poisons the row)
-        assert nloops == 2 and ld > n1 and x.dtype == np.float32
-        xp = np.full((n0, ld), np.nan, dtype=np.float32)
+    if ld and ld != n1:  # rows at stride ld; the padding columns hold poison (NaN / a huge int) that a read would show
+        assert nloops == 2 and ld > n1
+        xp = np.full((n0, ld), np.nan if x.dtype.kind == "f" else np.iinfo(x.dtype).max // 3, dtype=x.dtype)
         xp[:, :n1] = x.reshape(n0, n1)
         x_dev_src = xp.reshape(-1)
     else:
@@ -386,6 +386,36 @@ def test_flat_8byte_elements(H, torch_mod, oracle, dt, mis):
             res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis)
             assert res["kernel"] == "flat_tma"
             compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64", "i32", "i64"])
+def test_rowwise_dtypes_and_ops(H, torch_mod, oracle, dt):
+    """SUM / MIN / MAX over fp32, fp64, int32 and int64 rows (SURVEY §8(b)
+    ops and dtypes) on the fused row-wise kernel, aligned and ragged: rows
+    (fp: within the §8(c) tolerance, MIN/MAX and integers exact), owner map
+    and every level's partials vs the oracle.  fp32 sums keep the fp32 lane /
+    warp tree; the others carry 64-bit partials through 8-byte DSMEM slots."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c2_nest()
+    rng = np.random.default_rng(77)
+    for n0, n1, ld, mis, K, W, C in ((50, 4096, 4096, 0, 2, 4, 7), (21, 1001, 1003, 8, 4, 8, 3),
+                                     (13, 1000, 1000, 0, 2, 8, 5), (7, 5, 6, 0, 2, 4, 3)):
+        if dt == "f32":  # the workload's nonnegative values: reading #6 bounds the fp32 tree relative to sum |x|
+            x = gen.gen_f32(gen.SEED_C2, 0, n0 * n1)
+        elif dt == "f64":
+            x = rng.standard_normal(n0 * n1)
+        elif dt == "i32":
+            x = rng.integers(-(1 << 31), (1 << 31) - 1, n0 * n1, dtype=np.int64).astype(np.int32)
+        else:
+            x = rng.integers(-(1 << 62), 1 << 62, n0 * n1, dtype=np.int64)
+        if mis % x.itemsize:
+            mis = 0
+        for op in (H.OP_SUM, H.OP_MIN, H.OP_MAX):
+            res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=True, op=op, C=C, K=K, W=W, ld=ld,
+                           misalign=mis)
+            assert res["kernel"] == "rowwise_tma_dsmem", (dt, op, n1)
+            compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, op=op, C=C, K=K, W=W)
 
 
 def test_rowwise_fused_kernel_small(H, torch_mod, oracle):
