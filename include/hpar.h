@@ -168,7 +168,8 @@ typedef enum {
 typedef struct {
   int32_t first, last; /* hardware level range, HPAR_GPU <= first <= last <= HPAR_LANE */
   int32_t schedule;    /* hpar_schedule                                                  */
-  int32_t loop;        /* 0 or 1                                                         */
+  int32_t loop;        /* 0 or 1; 2 = the collapsed (row, nonzero) space of a CSR
+                          nest (the fused CSR kernels, reading #14) */
   int64_t chunk;       /* STATIC_CHUNK / DYNAMIC chunk (>= 1)                            */
   int64_t fanout;      /* tasks per parent; 0 = derived                                  */
   int32_t width;       /* partition width of `last`, 0 = none                            */

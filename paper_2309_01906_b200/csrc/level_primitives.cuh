@@ -41,6 +41,16 @@ struct OpT<OP_MAX, double> {
   __device__ __forceinline__ static double combine(double a, double b) { return b > a ? b : a; }
 };
 template <>
+struct OpT<OP_MIN, float> {
+  __device__ __forceinline__ static float identity() { return __int_as_float(0x7F800000); }
+  __device__ __forceinline__ static float combine(float a, float b) { return b < a ? b : a; }
+};
+template <>
+struct OpT<OP_MAX, float> {
+  __device__ __forceinline__ static float identity() { return __int_as_float(0xFF800000); }
+  __device__ __forceinline__ static float combine(float a, float b) { return b > a ? b : a; }
+};
+template <>
 struct OpT<OP_MIN, long long> {
   __device__ __forceinline__ static long long identity() { return 0x7FFFFFFFFFFFFFFFll; }
   __device__ __forceinline__ static long long combine(long long a, long long b) { return b < a ? b : a; }

@@ -41,6 +41,9 @@ cudaError_t launch_segmented(const NestArgs& a, void* wsbuf, int64_t ws_nnz, int
                              const char** name);
 cudaError_t segmented_span_ok(const NestArgs& a, unsigned long long* scratch, cudaStream_t s, bool* ok,
                               bool* needs_sync);
+bool segrows_matches(const NestArgs& a, const char** why);
+size_t segrows_ws_bytes(int64_t nnz);
+cudaError_t launch_segrows(const NestArgs& a, void* wsbuf, int64_t ws_nnz, cudaStream_t s, const char** name);
 size_t segmented_ws_bytes(int64_t nnz);
 void segmented_ws_qrow(int64_t nnz, size_t* off, size_t* len);
 cudaError_t launch_affine_rank_fold(const void* gathered, int G, void* out, cudaStream_t s);
@@ -298,6 +301,8 @@ struct hpar_nest {
   void* seg_ws = nullptr;  // CSR segmented kernel workspace (grown on demand)
   int64_t* seg_off_ws = nullptr;  // shifted offsets for values off a 16-byte boundary (grown on demand)
   int64_t seg_off_rows = 0;
+  void* sr_ws = nullptr;   // CSR rows kernel (other ops / dtypes) workspace (grown on demand)
+  int64_t sr_ws_nnz = -1;
   size_t seg_ws_bytes = 0;
   int64_t seg_ws_nnz = -1;  // the nnz the workspace layout was built for (its capacity)
   float* halo_buf = nullptr;  // ghost exchange staging (grown on demand)
@@ -604,6 +609,7 @@ extern "C" hpar_status hpar_nest_destroy(hpar_nest_t n) {
     cudaFree(n->barrier_word);
     cudaFree(n->seg_ws);
     cudaFree(n->seg_off_ws);
+    cudaFree(n->sr_ws);
     cudaFree(n->gather_buf);
     cudaFree(n->halo_buf);
   }
@@ -921,6 +927,21 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
       n->seg_off_rows = A.n0 + 1;
     }
     e = launch_segmented(A, n->seg_ws, n->seg_ws_nnz, n->seg_off_ws, stream, &name);
+  } else if (segrows_matches(A, &why)) {
+    // CSR rows for the other ops / dtypes: the same nest, a segmented
+    // reduction per window (kernel_segrows.cu); workspace keyed on its nnz
+    const int64_t nnz = d->n1;
+    if (nnz > n->sr_ws_nnz) {
+      const size_t need = segrows_ws_bytes(nnz);
+      cudaFree(n->sr_ws);
+      n->sr_ws = nullptr;
+      n->sr_ws_nnz = -1;
+      cudaError_t ae = cudaMalloc(&n->sr_ws, need);
+      if (ae != cudaSuccess) return fail(HPAR_E_NOMEM, "CSR rows workspace (%zu B): %s", need, cudaGetErrorString(ae));
+      CUDA_TRY(cudaMemsetAsync(n->sr_ws, 0, need, stream));
+      n->sr_ws_nnz = nnz;
+    }
+    e = launch_segrows(A, n->sr_ws, n->sr_ws_nnz, stream, &name);
   } else if (teams_matches(A, &why)) {
     e = launch_teams(A, (int)n->W, stream, &name);
   } else if (collapsed) {

@@ -62,3 +62,11 @@ for op, on in ((H.OP_MIN, "min"), (H.OP_MAX, "max")):
     nest = H.Nest(nests.c3_fast_nest(), device=0)
     line(f"CSR f32 {on}, c3_fast_nest", nest, H.make_desc(v, out, n0=R, n1=NNZ, nloops=2, keyed=True, offsets=offs,
                                                           op=op), NNZ * 4 + (R + 1) * 8 + R * 4)
+for dt, odt, on in ((torch.float64, torch.float64, "f64 sum"), (torch.int32, torch.int64, "i32 sum"),
+                    (torch.int64, torch.int64, "i64 sum")):
+    vv = (v * 1000).to(dt)
+    o2 = torch.zeros(R, dtype=odt, device="cuda")
+    nest = H.Nest(nests.c3_fast_nest(), device=0)
+    line(f"CSR {on}, c3_fast_nest", nest, H.make_desc(vv, o2, n0=R, n1=NNZ, nloops=2, keyed=True, offsets=offs),
+         NNZ * vv.element_size() + (R + 1) * 8 + R * 8)
+    del vv

@@ -161,6 +161,47 @@ def test_segmented_bounds(env, oracle):
         assert (count.t.cpu().numpy() == 1).all()
 
 
+def test_segrows_bounds(env, oracle):
+    """The CSR rows kernel for other ops / dtypes (kernel_segrows.cu): fp64
+    values between poison (NaN) margins, also 8 bytes off a granule, rows
+    and coverage between canaries; long rows through the chunk list."""
+    torch, H, nests = env
+    rng = np.random.default_rng(41)
+    rows = 700
+    lens = np.where(rng.random(rows) < 0.01, rng.integers(4097, 40000, rows), rng.geometric(0.1, rows))
+    lens[::29] = 0
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(off[-1])
+    v = rng.standard_normal(nnz) + 2.0
+    offd = torch.from_numpy(off).cuda()
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=3)
+    for shift, op in ((0, H.OP_SUM), (1, H.OP_MIN), (1, H.OP_SUM)):
+        _, vd = poisoned_input(torch, v, shift)
+        out = Canaried(torch, (rows,), torch.float64)
+        owner = Canaried(torch, (nnz,), torch.int64, fill=-1)
+        count = Canaried(torch, (nnz,), torch.int32)
+        nest.parallel_for_reduce(H.make_desc(vd, out.t, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd, op=op,
+                                             out_dtype=H.F64, verify=H.VERIFY_COVERAGE, owner=owner.t,
+                                             count=count.t))
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "segrows_csr"
+        for c in (out, owner, count):
+            c.check(torch)
+        got = out.t.cpu().numpy()
+        if op == H.OP_SUM:
+            assert_rel(got, oracle.nest_run(_c3_oracle_levels(oracle, nests), n0=rows, offsets=off, x=v, op=op,
+                                            keyed=True, coverage=False, partials=False).result)
+        else:
+            assert np.array_equal(got, oracle.nest_run(_c3_oracle_levels(oracle, nests), n0=rows, offsets=off, x=v,
+                                                       op=op, keyed=True, coverage=False, partials=False).result)
+        assert (count.t.cpu().numpy() == 1).all()
+
+
+def _c3_oracle_levels(oracle, nests):
+    from tests.nestutil import oracle_levels
+    return oracle_levels(oracle, nests.c3_nest(with_gpu=False, rows_chunk=16, width=8), 1, 2, 2, 4)
+
+
 def test_generic_bounds(env, oracle):
     torch, H, nests = env
     off = gen.csr_offsets(300, 4000)

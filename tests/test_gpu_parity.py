@@ -598,6 +598,64 @@ def test_segmented_misaligned_values(H, torch_mod, oracle, case, mis):
         assert_rel(out.cpu().numpy().astype(np.float64), oracle.segsum_f32(v, off))
 
 
+@pytest.mark.parametrize("dt,op", [("f32", "min"), ("f32", "max"), ("f64", "sum"), ("f64", "min"), ("i32", "sum"),
+                                   ("i64", "sum"), ("i64", "max")])
+@pytest.mark.parametrize("case", ["zipf", "all_empty", "one_huge_row", "edges", "short_only", "unaligned_tail"])
+def test_segrows_ops_and_dtypes(H, torch_mod, oracle, case, dt, op):
+    """The collapsed CSR nest (c3_fast_nest) for the ops and dtypes the fp32
+    sum kernel does not take (kernel_segrows.cu): every row vs the oracle's
+    nest walk (MIN/MAX and integers exact, fp64 within the tolerance; empty
+    rows the identity), every nonzero visited once, each block's short rows
+    on one warp; the long rows (> 4096) through the chunk list."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    off = dict(_csr_cases())[case]
+    rows, nnz = off.size - 1, int(off[-1])
+    rng = np.random.default_rng(12)
+    if dt == "f32":
+        v = gen.gen_f32(gen.SEED_C3, 0, nnz) - np.float32(0.5)
+    elif dt == "f64":
+        v = rng.standard_normal(nnz) + 3.0
+    elif dt == "i32":
+        v = rng.integers(-(1 << 31), (1 << 31) - 1, nnz, dtype=np.int64).astype(np.int32)
+    else:
+        v = rng.integers(-(1 << 62), 1 << 62, nnz, dtype=np.int64)
+    hop = {"sum": H.OP_SUM, "min": H.OP_MIN, "max": H.OP_MAX}[op]
+    fp = dt in ("f32", "f64")
+    for lpl in (16, 8):
+        nest = H.Nest(nests.c3_fast_nest(lane_chunk=lpl), device=0, cluster_dim=2, warps_per_cta=8, clusters=5)
+        xd = torch.from_numpy(v).cuda() if nnz else torch.zeros(4, dtype=torch.from_numpy(v).dtype, device="cuda")
+        offd = torch.from_numpy(off).cuda()
+        out = torch.full((max(rows, 1),), -1, dtype=torch.float64 if fp else torch.int64, device="cuda")
+        owner = torch.full((max(nnz, 1),), -1, dtype=torch.int64, device="cuda")
+        count = torch.zeros(max(nnz, 1), dtype=torch.int32, device="cuda")
+        for verify in (0, H.VERIFY_COVERAGE):
+            out.fill_(-1)
+            d = H.make_desc(xd, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd, op=hop,
+                            out_dtype=H.F64 if fp else H.I64, verify=verify,
+                            owner=owner if verify else None, count=count if verify else None)
+            nest.parallel_for_reduce(d)
+            torch.cuda.synchronize()
+            assert nest.last_kernel() == "segrows_csr"
+            ref_levels = nests.c3_nest(with_gpu=False, rows_chunk=16, width=8)
+            o = oracle.nest_run(oracle_levels(oracle, ref_levels, 1, 2, 2, 4), n0=rows, offsets=off, x=v, op=hop,
+                                keyed=True, coverage=False, partials=False)
+            got = out.cpu().numpy()[:rows]
+            if fp and op == "sum":
+                assert_rel(got, o.result)
+            else:
+                assert np.array_equal(got, o.result), (case, dt, op)
+        if nnz:
+            assert (count.cpu().numpy()[:nnz] == 1).all()
+            own = owner.cpu().numpy()[:nnz] // 32
+            lens = np.diff(off)
+            for b0 in range(0, rows, 256):
+                rs = [r for r in range(b0, min(b0 + 256, rows)) if 0 < lens[r] <= 4096]
+                if rs:
+                    ws_ = np.concatenate([own[off[r]:off[r + 1]] for r in rs])
+                    assert (ws_ == ws_[0]).all(), "a block's short rows span several warps"
+
+
 def _probe_expect(oracle, level, C, K, W, rounds):
     """The oracle's fold for every task of the probe (hpar_barrier_probe):
     sum over rounds of the sum over the task's sibling group of
