@@ -56,6 +56,29 @@ def test_stress_segmented(env, oracle):
     assert nest.last_kernel() == "segmented_csr"
 
 
+def test_stress_segrows(env, oracle):
+    """The CSR rows kernel for other ops / dtypes: fp64 sums with long rows
+    (chunk list, last-chunk ordered fold, self-resetting tickets) bitwise
+    identical over repeated calls and equal to the oracle."""
+    torch, H, nests = env
+    from tests.nestutil import oracle_levels
+    rng = np.random.default_rng(19)
+    rows = 20000
+    lens = np.where(rng.random(rows) < 0.004, rng.integers(4097, 80000, rows), rng.geometric(0.07, rows))
+    lens[::13] = 0
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    v = rng.standard_normal(int(off[-1])) + 1.0
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8)
+    x, o = torch.from_numpy(v).cuda(), torch.from_numpy(off).cuda()
+    out = torch.empty(rows, dtype=torch.float64, device="cuda")
+    d = H.make_desc(x, out, n0=rows, n1=v.size, nloops=2, keyed=True, offsets=o, out_dtype=H.F64)
+    got = _repeat(torch, nest, d, out)
+    assert nest.last_kernel() == "segrows_csr"
+    ol = oracle_levels(oracle, nests.c3_nest(with_gpu=False, rows_chunk=16, width=8), 1, 2, 2, 4)
+    assert_rel(got, oracle.nest_run(ol, n0=rows, offsets=off, x=v, keyed=True, coverage=False,
+                                    partials=False).result)
+
+
 def test_stress_rowwise(env, oracle):
     torch, H, nests = env
     rows, cols = 3000, 4096
