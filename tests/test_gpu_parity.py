@@ -377,13 +377,13 @@ def test_flat_8byte_elements(H, torch_mod, oracle, dt, mis):
     levels = nests.c5_nest(K=2)
     C, K, W = 5, 2, 8
     rng = np.random.default_rng(64)
-    for n in (1, 3, 4096 * 2 * 5, 4096 * 2 * 7 + 4 * 99 + 3, 300001):
+    for n in (0, 1, 3, 4096 * 2 * 5, 4096 * 2 * 7 + 4 * 99 + 3, 300001):
         if dt == "f64":
             x = rng.standard_normal(n) * 1e3
         else:
             x = rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)
         for op in (H.OP_SUM, H.OP_MIN, H.OP_MAX):
-            res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis)
+            res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis if n else 0)
             assert res["kernel"] == "flat_tma"
             compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
 
@@ -654,6 +654,20 @@ def test_segrows_ops_and_dtypes(H, torch_mod, oracle, case, dt, op):
                 if rs:
                     ws_ = np.concatenate([own[off[r]:off[r + 1]] for r in rs])
                     assert (ws_ == ws_[0]).all(), "a block's short rows span several warps"
+
+
+def test_segrows_zero_rows(H, torch_mod):
+    """A CSR call with no rows on the CSR rows kernel: nothing written, both
+    launches exit at once (the block ticket and the empty chunk list)."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=3)
+    x = torch.zeros(4, dtype=torch.float64, device="cuda")
+    out = torch.full((1,), -3.0, dtype=torch.float64, device="cuda")
+    off = torch.zeros(1, dtype=torch.int64, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=0, n1=0, nloops=2, keyed=True, offsets=off, out_dtype=H.F64))
+    torch.cuda.synchronize()
+    assert out.item() == -3.0
 
 
 def _probe_expect(oracle, level, C, K, W, rounds):
