@@ -111,10 +111,10 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
                 acc += (long long)v.x + (long long)v.y + (long long)v.z + (long long)v.w;
               }
             } else {
-              acc = OpT<OP, Acc>::combine(acc, (Acc)v.x);
-              acc = OpT<OP, Acc>::combine(acc, (Acc)v.y);
-              acc = OpT<OP, Acc>::combine(acc, (Acc)v.z);
-              acc = OpT<OP, Acc>::combine(acc, (Acc)v.w);
+              acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(v.x));
+              acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(v.y));
+              acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(v.z));
+              acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(v.w));
             }
             if constexpr (VERIFY) {
               for (int q = 0; q < 4; ++q) {
@@ -145,10 +145,13 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
             if constexpr (OP == OP_SUM) {
               acc += (lo.x + lo.y) + (hi.x + hi.y);  // integers: two's complement, wraps mod 2^64
             } else {
-              acc = OpT<OP, Acc>::combine(acc, (Acc)lo.x);
-              acc = OpT<OP, Acc>::combine(acc, (Acc)lo.y);
-              acc = OpT<OP, Acc>::combine(acc, (Acc)hi.x);
-              acc = OpT<OP, Acc>::combine(acc, (Acc)hi.y);
+              // a tree over the four (associative: the same result as the
+              // in-order fold, also for the ordered AFFINE op) keeps the
+              // dependent chain on acc to one combine per vector
+              using E = ElemT<OP, Acc, In>;
+              using O = OpT<OP, Acc>;
+              acc = O::combine(acc, O::combine(O::combine(E::make(lo.x), E::make(lo.y)),
+                                               O::combine(E::make(hi.x), E::make(hi.y))));
             }
             if constexpr (VERIFY) {
               for (int q = 0; q < 4; ++q) {
@@ -174,10 +177,10 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
               }
             } else {
               const In* e = st + 4 * f;
-              acc = OpT<OP, Acc>::combine(acc, (Acc)e[0]);
-              acc = OpT<OP, Acc>::combine(acc, (Acc)e[1]);
-              acc = OpT<OP, Acc>::combine(acc, (Acc)e[2]);
-              acc = OpT<OP, Acc>::combine(acc, (Acc)e[3]);
+              acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[0]));
+              acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[1]));
+              acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[2]));
+              acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[3]));
             }
             if constexpr (VERIFY) {
               for (int q = 0; q < 4; ++q) {
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
             const int64_t off = 4 * (int64_t)f + q;
             if (off >= len) break;
             const In e = (off < in_smem) ? st[off] : x[base + off];
-            acc = OpT<OP, Acc>::combine(acc, (Acc)e);
+            acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e));
             if constexpr (VERIFY) {
               const int64_t it = base + off;
               if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
@@ -261,7 +264,8 @@ cudaError_t launch_v(const NestArgs& a, int W, int tile, cudaStream_t s) {
 // Does the nest have the coalesced flat shape (and the call suit the kernel)?
 bool flat_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 1 || a.keyed) { *why = "not a flat total"; return false; }
-  if (a.op == OP_HIST || a.op == OP_AFFINE) { *why = "sum/min/max only"; return false; }
+  if (a.op == OP_HIST) { *why = "sum/min/max/affine only"; return false; }
+  if (a.op == OP_AFFINE && a.in_dtype != DT_I64) { *why = "affine: int64 input"; return false; }
   if (a.in_dtype != DT_F32 && a.in_dtype != DT_I32 && a.in_dtype != DT_F64 && a.in_dtype != DT_I64) {
     *why = "dtype";
     return false;
@@ -303,6 +307,7 @@ cudaError_t launch_flat(const NestArgs& a, int W, cudaStream_t s, const char** n
     if (a.op == OP_MAX) return launch_v<double, double, OP_MAX>(a, W, tile, s);
   } else if (a.in_dtype == DT_I64) {
     if (a.op == OP_SUM) return launch_v<long long, long long, OP_SUM>(a, W, tile, s);
+    if (a.op == OP_AFFINE) return launch_v<long long, Aff, OP_AFFINE>(a, W, tile, s);
     if (a.op == OP_MIN) return launch_v<long long, long long, OP_MIN>(a, W, tile, s);
     if (a.op == OP_MAX) return launch_v<long long, long long, OP_MAX>(a, W, tile, s);
   } else {

@@ -70,3 +70,12 @@ for dt, odt, on in ((torch.float64, torch.float64, "f64 sum"), (torch.int32, tor
     line(f"CSR {on}, c3_fast_nest", nest, H.make_desc(vv, o2, n0=R, n1=NNZ, nloops=2, keyed=True, offsets=offs),
          NNZ * vv.element_size() + (R + 1) * 8 + R * 8)
     del vv
+# the ordered AFFINE op (NEXT f2) on a flat nest of int64
+x = torch.randint(-(1 << 62), 1 << 62, (n,), dtype=torch.int64, device="cuda")
+out = torch.zeros(2, dtype=torch.int64, device="cuda")
+nest = H.Nest(nests.c5_nest(2), device=0, cluster_dim=2, warps_per_cta=4, clusters=148)
+line("flat i64 affine 2^28", nest, H.make_desc(x, out, n0=n, op=H.OP_AFFINE), n * 8)
+lv = nests.c5_nest(2)
+lv[-1].chunk = 2  # lane static(2): not the fused flat shape -> the generic interpreter
+nest = H.Nest(lv, device=0, cluster_dim=2, warps_per_cta=4, clusters=148)
+line("flat i64 affine 2^28, lane static(2)", nest, H.make_desc(x, out, n0=n, op=H.OP_AFFINE), n * 8)

@@ -388,6 +388,25 @@ def test_flat_8byte_elements(H, torch_mod, oracle, dt, mis):
             compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
 
 
+@pytest.mark.parametrize("mis", [0, 8])
+def test_flat_affine_op(H, torch_mod, oracle, mis):
+    """The ordered AFFINE operator (NEXT f2) on the fused flat kernel: the
+    lane folds its elements in ascending position order and every level
+    folds its children in ascending task order, which is the nest's fold
+    (the oracle's nest walk); result, owner map and every level's partials
+    bit-exact, aligned and 8 bytes off a granule."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c5_nest(K=2)
+    C, K, W = 5, 2, 8
+    rng = np.random.default_rng(65)
+    for n in (1, 4096 * 2 * 5 + 1, 4096 * 2 * 7 + 4 * 99 + 3, 200001):
+        x = rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)
+        res = run_nest(H, torch, levels, x, n0=n, op=H.OP_AFFINE, C=C, K=K, W=W, misalign=mis)
+        assert res["kernel"] == "flat_tma"
+        compare(oracle, H, levels, res, x, n0=n, op=H.OP_AFFINE, C=C, K=K, W=W)
+
+
 @pytest.mark.parametrize("dt", ["f32", "f64", "i32", "i64"])
 def test_rowwise_dtypes_and_ops(H, torch_mod, oracle, dt):
     """SUM / MIN / MAX over fp32, fp64, int32 and int64 rows (SURVEY §8(b)
