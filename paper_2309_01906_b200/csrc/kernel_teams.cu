@@ -46,10 +46,10 @@ __global__ void __launch_bounds__(1024) teams_kernel(const __grid_constant__ Nes
       for (int k = 0; k < G; ++k) {
         if (row + k < row0 + nrow) {
           const In* e = (const In*)&v[k];
-          acc = OpT<OP, Acc>::combine(acc, (Acc)e[0]);
-          acc = OpT<OP, Acc>::combine(acc, (Acc)e[1]);
-          acc = OpT<OP, Acc>::combine(acc, (Acc)e[2]);
-          acc = OpT<OP, Acc>::combine(acc, (Acc)e[3]);
+          acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[0]));
+          acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[1]));
+          acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[2]));
+          acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[3]));
         }
       }
     }
@@ -62,13 +62,13 @@ __global__ void __launch_bounds__(1024) teams_kernel(const __grid_constant__ Nes
         if constexpr (sizeof(In) == 4) {
           const int4 v = *(const int4*)(xr + base);
           const In* e = (const In*)&v;
-          acc = OpT<OP, Acc>::combine(acc, (Acc)e[0]);
-          acc = OpT<OP, Acc>::combine(acc, (Acc)e[1]);
-          acc = OpT<OP, Acc>::combine(acc, (Acc)e[2]);
-          acc = OpT<OP, Acc>::combine(acc, (Acc)e[3]);
+          acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[0]));
+          acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[1]));
+          acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[2]));
+          acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e[3]));
         }
       } else {
-        for (int64_t col = base; col < end; ++col) acc = OpT<OP, Acc>::combine(acc, (Acc)xr[col]);
+        for (int64_t col = base; col < end; ++col) acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(xr[col]));
       }
       if constexpr (VERIFY) {
         for (int64_t col = base; col < end; ++col) {
@@ -108,7 +108,8 @@ cudaError_t launch_t(const NestArgs& a, int W, int chunk, cudaStream_t s) {
 
 bool teams_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 2 || a.keyed || a.offsets) { *why = "not a dense 2-loop total"; return false; }
-  if (a.op == OP_HIST || a.op == OP_AFFINE) { *why = "sum/min/max only"; return false; }
+  if (a.op == OP_HIST) { *why = "sum/min/max/affine only"; return false; }
+  if (a.op == OP_AFFINE && a.in_dtype != DT_I64) { *why = "affine: int64 input"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
   LevelView v = device_levels(a);
   if (v.n != 2) { *why = "needs teams and threads levels"; return false; }
@@ -140,6 +141,7 @@ cudaError_t launch_teams(const NestArgs& a, int W, cudaStream_t s, const char** 
       return launch_t<float, double, OP_MAX>(a, W, chunk, s);
     case DT_I64:
       if (a.op == OP_SUM) return launch_t<long long, long long, OP_SUM>(a, W, chunk, s);
+      if (a.op == OP_AFFINE) return launch_t<long long, Aff, OP_AFFINE>(a, W, chunk, s);
       if (a.op == OP_MIN) return launch_t<long long, long long, OP_MIN>(a, W, chunk, s);
       return launch_t<long long, long long, OP_MAX>(a, W, chunk, s);
     default:

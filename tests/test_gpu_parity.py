@@ -796,6 +796,23 @@ def test_ordered_affine_op(H, torch_mod, oracle):
     compare(oracle, H, levels, res, x, n0=29, n1=333, keyed=True, op=H.OP_AFFINE, C=3, K=2, W=2)
 
 
+def test_teams_affine_op(H, torch_mod, oracle):
+    """The ordered AFFINE op on the teams x threads kernel (config-1 nest,
+    int64): each thread folds its (row, chunk) iterations in nest order and
+    every level in ascending task order — results, owner map and partials
+    bit-exact vs the oracle's nest fold, for chunk 4 and a ragged chunk."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    rng = np.random.default_rng(3)
+    for n0, n1, chunk, C in ((64, 1024, 4, 8), (37, 1000, 3, 5), (5, 7, 4, 3)):
+        levels = nests.c1_nest(outer=0)
+        levels[-1].chunk = chunk
+        x = rng.integers(-(1 << 62), 1 << 62, n0 * n1, dtype=np.int64)
+        res = run_nest(H, torch, levels, x, n0=n0, n1=n1, op=H.OP_AFFINE, C=C, K=2, W=4)
+        assert res["kernel"] == "teams_threads"
+        compare(oracle, H, levels, res, x, n0=n0, n1=n1, op=H.OP_AFFINE, C=C, K=2, W=4)
+
+
 def test_generic_keyed_dynamic_repeated_calls(H, torch_mod, oracle):
     """Regression: in keyed mode every CTA of a cluster must be done before the
     cluster's leader arrives at the grid ticket (whose last arriver resets the
