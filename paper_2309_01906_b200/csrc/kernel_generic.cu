@@ -42,6 +42,31 @@ __device__ __forceinline__ int64_t chain_map(const Chain& ch, int lo, int hi, co
   return j;
 }
 
+// chain_map plus the run length: positions j .. j+run-1 of the list after
+// level hi-1 map to consecutive positions of the list before level lo (every
+// level keeps them inside one of its chunks / its block), so an iteration
+// loop maps once per run and then steps by one — the same visit order.
+__device__ __forceinline__ int64_t chain_map_run(const Chain& ch, int lo, int hi, const int64_t* lens, int64_t j,
+                                                 int64_t* run) {
+  int64_t r = lens[hi] - j;
+  for (int k = hi - 1; k >= lo; --k) {
+    const int s = ch.sched[k];
+    if (s == SCHED_STATIC) {
+      const int64_t left = lens[k + 1] - j;
+      r = left < r ? left : r;
+    } else if (s == SCHED_NONE) {
+      r = 1;
+    } else {
+      const int64_t c = ch.chunk[k];
+      const int64_t left = c - j % c;
+      r = left < r ? left : r;
+    }
+    j = own_map(s, ch.chunk[k], lens[k], ch.T[k], ch.t[k], j);
+  }
+  *run = r > 0 ? r : 1;
+  return j;
+}
+
 template <typename Acc>
 struct Shared {
   Acc warp[2][32];
@@ -167,10 +192,14 @@ struct Generic {
     int64_t lens[kMaxLev + 1];
     chain_lens(c1, 0, c1.m, row_len(i), lens);
     const int64_t cnt = lens[c1.m];
-    for (int64_t q = 0; q < cnt; ++q) {
-      const int64_t j = chain_map(c1, 0, c1.m, lens, q);
-      acc = OpT<OP, Acc>::combine(acc, load(i, j));
-      record(iter_index(i, j));
+    for (int64_t q = 0; q < cnt;) {
+      int64_t run;
+      const int64_t j0 = chain_map_run(c1, 0, c1.m, lens, q, &run);
+      for (int64_t u = 0; u < run; ++u) {
+        acc = OpT<OP, Acc>::combine(acc, load(i, j0 + u));
+        record(iter_index(i, j0 + u));
+      }
+      q += run;
     }
     return acc;
   }
@@ -277,7 +306,12 @@ struct Generic {
     if (dyn0 < 0) {
       chain_lens(c0, 0, c0.m, a.n0, lens);
       const int64_t cnt = lens[c0.m];
-      for (int64_t q = 0; q < cnt; ++q) visit_row(chain_map(c0, 0, c0.m, lens, q));
+      for (int64_t q = 0; q < cnt;) {
+        int64_t run;
+        const int64_t i0 = chain_map_run(c0, 0, c0.m, lens, q, &run);
+        for (int64_t u = 0; u < run; ++u) visit_row(i0 + u);
+        q += run;
+      }
     } else {
       // levels above the dynamic one are static: their list is fixed
       chain_lens(c0, 0, dyn0, a.n0, lens);
@@ -294,9 +328,13 @@ struct Generic {
         const int64_t len_m = (n_up - m * c < c) ? (n_up - m * c) : c;
         chain_lens(c0, dyn0 + 1, c0.m, len_m, lensl);
         const int64_t cnt = lensl[c0.m];
-        for (int64_t q = 0; q < cnt; ++q) {
-          const int64_t p = chain_map(c0, dyn0 + 1, c0.m, lensl, q) + m * c;
-          visit_row(chain_map(c0, 0, dyn0, lens, p));
+        for (int64_t q = 0; q < cnt;) {
+          int64_t run1, run2;
+          const int64_t p = chain_map_run(c0, dyn0 + 1, c0.m, lensl, q, &run1) + m * c;
+          const int64_t i0 = chain_map_run(c0, 0, dyn0, lens, p, &run2);
+          const int64_t run = run1 < run2 ? run1 : run2;
+          for (int64_t u = 0; u < run; ++u) visit_row(i0 + u);
+          q += run;
         }
       }
     }
