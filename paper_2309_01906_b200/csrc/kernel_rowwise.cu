@@ -76,12 +76,22 @@ int64_t rowwise_stage_bytes(const NestArgs& a) {
 // partial and the DSMEM slot (fp32 for fp32 sums — the fp32 tree of reading
 // #4 — else the 64-bit accumulator); X: the combiner's and the exported
 // partials' type (fp64 for floating point, int64 for integers).
-template <typename In> struct RwX { using T = long long; };
-template <> struct RwX<float> { using T = double; };
-template <> struct RwX<double> { using T = double; };
+template <typename In, int OP> struct RwX { using T = long long; };
+template <int OP> struct RwX<float, OP> { using T = double; };
+template <int OP> struct RwX<double, OP> { using T = double; };
+template <> struct RwX<long long, OP_AFFINE> { using T = Aff; };  // the ordered op (NEXT f2)
 template <typename In, int OP>
 using RwP = typename std::conditional<std::is_same<In, float>::value && OP == OP_SUM, float,
-                                      typename RwX<In>::T>::type;
+                                      typename RwX<In, OP>::T>::type;
+
+// xor shuffles that also move the 16-byte ordered accumulator; lane 0's
+// butterfly combines (own, higher lanes) at every step: the ordered tree
+template <typename T>
+__device__ __forceinline__ T shfl_xor_t(T v, int off) { return __shfl_xor_sync(0xffffffffu, v, off); }
+template <>
+__device__ __forceinline__ Aff shfl_xor_t<Aff>(Aff v, int off) {
+  return Aff{__shfl_xor_sync(0xffffffffu, v.a, off), __shfl_xor_sync(0xffffffffu, v.b, off)};
+}
 
 // the four elements of lane vector f (elements 4f .. 4f+3 of the CTA's
 // block), from a ring stage whose data start `mis` bytes into its first
@@ -120,9 +130,17 @@ __device__ __forceinline__ void st_async_part(uint32_t addr, uint32_t bar, long 
                "r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void st_async_part(uint32_t addr, uint32_t bar, Aff v) {  // two 8-byte transactions
+  st_async_part(addr, bar, (long long)v.a);
+  st_async_part(addr + 8, bar, (long long)v.b);
+}
 
 template <typename X>
 __device__ __forceinline__ void store_row(const NestArgs& a, int64_t row, X v) {
+  if constexpr (std::is_same<X, Aff>::value) {
+    ((Aff*)a.out)[row] = v;  // u64 [rows][2]
+    return;
+  } else
   switch (a.out_dtype) {
     case DT_F32: ((float*)a.out)[row] = (float)v; break;
     case DT_F64: ((double*)a.out)[row] = (double)v; break;
@@ -134,7 +152,7 @@ template <typename In, int OP, bool VERIFY, int NV>
 __global__ void __launch_bounds__(1024, 1)
     rowwise_kernel(const __grid_constant__ NestArgs a, int W, int qcols, int kStages, int stage_bytes) {
   using P = RwP<In, OP>;
-  using X = typename RwX<In>::T;
+  using X = typename RwX<In, OP>::T;
   constexpr bool F32SUM = std::is_same<P, float>::value;
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
@@ -210,11 +228,11 @@ __global__ void __launch_bounds__(1024, 1)
           v = (X)slot[s][e];
         }
         // warp partials -> CTA partials (every W lanes), ordered
-        for (int off = 1; off < W; off <<= 1) v = OpT<OP, X>::combine(v, __shfl_xor_sync(0xffffffffu, v, off));
+        for (int off = 1; off < W; off <<= 1) v = OpT<OP, X>::combine(v, shfl_xor_t(v, off));
         if (VERIFY && live && (a.verify & V_PARTIALS) && (e % W) == 0)
           export_slot<X>(a, S_CTA, (row0 + j) * K + e / W, v);
         // CTA partials -> row (cluster), ordered
-        for (int off = W; off < npush; off <<= 1) v = OpT<OP, X>::combine(v, __shfl_xor_sync(0xffffffffu, v, off));
+        for (int off = W; off < npush; off <<= 1) v = OpT<OP, X>::combine(v, shfl_xor_t(v, off));
         if (live && e == 0) store_row<X>(a, row0 + j, v);
         // free the slot in every CTA of the cluster (relaxed: it orders only
         // the slot reads above, which the shuffles have consumed)
@@ -248,7 +266,7 @@ __global__ void __launch_bounds__(1024, 1)
           load_quad<In, (NV < 0)>(stage, f, mis, e);
           P t[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) t[k] = (P)e[k];
+          for (int k = 0; k < 4; ++k) t[k] = ElemT<OP, P, In>::make(e[k]);
           if constexpr (NV < 0) {
             const int rem = lenk - 4 * f;  // the last vector may be partial: identities keep the tree's order
 #pragma unroll
@@ -278,7 +296,7 @@ __global__ void __launch_bounds__(1024, 1)
           export_slot<X>(a, S_LANE_IN, (row0 + j) * (int64_t)(npush * 32) + push_idx * 32 + lane, (X)acc);
       }
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) acc = OpT<OP, P>::combine(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+      for (int off = 1; off < 32; off <<= 1) acc = OpT<OP, P>::combine(acc, shfl_xor_t(acc, off));
       if (lane == 0) {
         if constexpr (VERIFY) {
           if (a.verify & V_PARTIALS) export_slot<X>(a, S_WARP, (row0 + j) * npush + push_idx, (X)acc);
@@ -344,6 +362,11 @@ cudaError_t launch_op(const NestArgs& a, int W, int qcols, int stages, int stage
                           : launch_nv<In, OP_MIN, false>(a, W, qcols, stages, stage_bytes, s);
     case OP_MAX: return v ? launch_nv<In, OP_MAX, true>(a, W, qcols, stages, stage_bytes, s)
                           : launch_nv<In, OP_MAX, false>(a, W, qcols, stages, stage_bytes, s);
+    case OP_AFFINE:
+      if constexpr (std::is_same<In, long long>::value)
+        return v ? launch_nv<In, OP_AFFINE, true>(a, W, qcols, stages, stage_bytes, s)
+                 : launch_nv<In, OP_AFFINE, false>(a, W, qcols, stages, stage_bytes, s);
+      return cudaErrorInvalidValue;
     default: return cudaErrorInvalidValue;
   }
 }
@@ -367,7 +390,11 @@ int rowwise_stages(int stage_bytes) {
 
 bool rowwise_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 2 || !a.keyed || a.offsets) { *why = "not a dense keyed 2-loop nest"; return false; }
-  if (a.op != OP_SUM && a.op != OP_MIN && a.op != OP_MAX) { *why = "rowwise kernel: sum / min / max"; return false; }
+  if (a.op != OP_SUM && a.op != OP_MIN && a.op != OP_MAX && a.op != OP_AFFINE) {
+    *why = "rowwise kernel: sum / min / max / affine";
+    return false;
+  }
+  if (a.op == OP_AFFINE && a.in_dtype != DT_I64) { *why = "affine: int64 input"; return false; }
   if (a.in_dtype != DT_F32 && a.in_dtype != DT_F64 && a.in_dtype != DT_I32 && a.in_dtype != DT_I64) {
     *why = "rowwise kernel: dtype";
     return false;

@@ -437,6 +437,25 @@ def test_rowwise_dtypes_and_ops(H, torch_mod, oracle, dt):
             compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, op=op, C=C, K=K, W=W)
 
 
+def test_rowwise_affine_op(H, torch_mod, oracle):
+    """The ordered AFFINE op per row (keyed, int64) on the fused row-wise
+    kernel: lane 0 of every butterfly combines (own, higher lanes), the
+    combiner folds warp partials and CTA partials in ascending order, 16-byte
+    partials travel as two 8-byte st.async transactions.  Rows, owner map and
+    every level's partials bit-exact vs the oracle's nest fold, aligned and
+    ragged."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    levels = nests.c2_nest()
+    rng = np.random.default_rng(99)
+    for n0, n1, ld, mis, K, W, C in ((40, 4096, 4096, 0, 2, 4, 7), (21, 1001, 1003, 8, 4, 8, 3), (7, 5, 6, 0, 2, 4, 3)):
+        x = rng.integers(-(1 << 62), 1 << 62, n0 * n1, dtype=np.int64)
+        res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=True, op=H.OP_AFFINE, C=C, K=K, W=W, ld=ld,
+                       misalign=mis)
+        assert res["kernel"] == "rowwise_tma_dsmem"
+        compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, op=H.OP_AFFINE, C=C, K=K, W=W)
+
+
 def test_rowwise_fused_kernel_small(H, torch_mod, oracle):
     """The fused row-wise kernel (config-2 nest) on 50 x 4096 and ragged
     columns: rows, owner map, per-row lane/warp/CTA partials vs oracle."""
