@@ -57,13 +57,33 @@ struct SegRowsWS {
   int64_t cap_ent, cap_chunks;
 };
 
-template <typename In>
+template <typename In, int OP>
 struct SrX {
   using T = typename std::conditional<std::is_floating_point<In>::value, double, long long>::type;
 };
+template <>
+struct SrX<long long, OP_AFFINE> {  // the ordered op (NEXT f2): every fold below is order-preserving
+  using T = Aff;
+};
+template <typename T>
+__device__ __forceinline__ T shfl_up_t(T v, int off) { return __shfl_up_sync(0xffffffffu, v, off); }
+template <>
+__device__ __forceinline__ Aff shfl_up_t<Aff>(Aff v, int off) {
+  return Aff{__shfl_up_sync(0xffffffffu, v.a, off), __shfl_up_sync(0xffffffffu, v.b, off)};
+}
+template <typename T>
+__device__ __forceinline__ T shfl_idx_t(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+template <>
+__device__ __forceinline__ Aff shfl_idx_t<Aff>(Aff v, int src) {
+  return Aff{__shfl_sync(0xffffffffu, v.a, src), __shfl_sync(0xffffffffu, v.b, src)};
+}
 
 template <typename X>
 __device__ __forceinline__ void sr_store(const NestArgs& a, int64_t row, X v) {
+  if constexpr (std::is_same<X, Aff>::value) {
+    ((Aff*)a.out)[row] = v;  // u64 [rows][2]
+    return;
+  } else
   switch (a.out_dtype) {
     case DT_F32: ((float*)a.out)[row] = (float)v; break;
     case DT_F64: ((double*)a.out)[row] = (double)v; break;
@@ -94,12 +114,17 @@ __device__ __forceinline__ void gran_elems(const int4 r, In (&e)[16 / sizeof(In)
   }
 }
 
+// the window fold type: fp64 / int64 sums, the affine pair; fp32 MIN/MAX
+// stay fp32 (exact)
+template <typename In, int OP>
+using SrFold = typename std::conditional<std::is_same<In, float>::value && OP != OP_SUM, float,
+                                         typename SrX<In, OP>::T>::type;
+
 template <typename In, int OP, int LPL, bool VERIFY>
 __global__ void __launch_bounds__(SR_WARPS * 32, SR_MINB) segrows_blocks(const __grid_constant__ NestArgs a, SegRowsWS ws) {
-  // X: the fold type (fp64 / int64 sums; fp32 MIN/MAX stay fp32, exact)
-  using X = typename std::conditional<std::is_same<In, float>::value && OP != OP_SUM, float,
-                                      typename SrX<In>::T>::type;
+  using X = SrFold<In, OP>;
   using O = OpT<OP, X>;
+  using E = ElemT<OP, X, In>;
   constexpr int WIN = 32 * LPL;
   // dynamic: per warp the block's offsets, then the window's folds (padded:
   // lane-major rows of LPL + 1 values, conflict-free)
@@ -116,7 +141,7 @@ __global__ void __launch_bounds__(SR_WARPS * 32, SR_MINB) segrows_blocks(const _
   const int64_t R = a.n0;
   const int64_t nblocks = (R + SR_RB - 1) / SR_RB;
   long long* off = (long long*)sr_dsm + (size_t)warp * (SR_RB + 1);
-  X* S = (X*)((long long*)sr_dsm + (size_t)SR_WARPS * (SR_RB + 1)) + (size_t)warp * 32 * (LPL + 1);
+  X* S = (X*)((long long*)sr_dsm + (size_t)SR_WARPS * (SR_RB + 1)) + (size_t)warp * 32 * (LPL + 1);  // 8-byte aligned
   const int64_t leaf0 = (int64_t)a.rank * a.threads_per_gpu + ((int64_t)blockIdx.x * SR_WARPS + warp) * 32;
   auto cover = [&](int64_t p, int64_t who) {
     if constexpr (VERIFY) {
@@ -194,14 +219,14 @@ __global__ void __launch_bounds__(SR_WARPS * 32, SR_MINB) segrows_blocks(const _
 #pragma unroll
             for (int t = 0; t < VEC; ++t) {
               const long long q = q0 + t;
-              v[g * VEC + t] = (q >= P0 && q < we) ? (X)e[t] : O::identity();
+              v[g * VEC + t] = (q >= P0 && q < we) ? E::make(e[t]) : O::identity();
             }
           }
         } else {
 #pragma unroll
           for (int k = 0; k < LPL; ++k) {
             const long long q = w + LPL * lane + k;
-            v[k] = q < we ? (X)__ldg(x + q) : O::identity();
+            v[k] = q < we ? E::make(__ldg(x + q)) : O::identity();
           }
         }
         // pass A: row heads (empty rows mark the next row's head: harmless)
@@ -233,10 +258,10 @@ __global__ void __launch_bounds__(SR_WARPS * 32, SR_MINB) segrows_blocks(const _
         X y = run;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const X t = __shfl_up_sync(0xffffffffu, y, o);
+          const X t = shfl_up_t(y, o);
           if (o <= lim) y = O::combine(t, y);
         }
-        X cin = __shfl_up_sync(0xffffffffu, y, 1);
+        X cin = shfl_up_t(y, 1);
         if (lane == 0) cin = O::identity();
         s_cin[warp][lane] = cin;
         s_fh[warp][lane] = hbits ? __ffs(hbits) - 1 : LPL;
@@ -268,7 +293,7 @@ __global__ void __launch_bounds__(SR_WARPS * 32, SR_MINB) segrows_blocks(const _
           const int cnt = __popc(vm);
           if (cnt == 0) break;
           if (!((cm >> (cnt - 1)) & 1u)) {  // the last overlapping row continues
-            carry = __shfl_sync(0xffffffffu, val, cnt - 1);
+            carry = shfl_idx_t(val, cnt - 1);
             rcur = r + cnt - 1;
             break;
           }
@@ -290,8 +315,9 @@ __global__ void __launch_bounds__(SR_WARPS * 32, SR_MINB) segrows_blocks(const _
 // row folds the row's chunk partials in ascending order.
 template <typename In, int OP, bool VERIFY>
 __global__ void __launch_bounds__(SR_WARPS * 32) segrows_long(const __grid_constant__ NestArgs a, SegRowsWS ws) {
-  using X = typename SrX<In>::T;
+  using X = typename SrX<In, OP>::T;
   using O = OpT<OP, X>;
+  using E = ElemT<OP, X, In>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const In* x = (const In*)a.in;
   X* part = (X*)ws.part;
@@ -309,7 +335,13 @@ __global__ void __launch_bounds__(SR_WARPS * 32) segrows_long(const __grid_const
     const long long p0 = en.start + j * SR_CHUNK;
     const long long p1 = (en.start + en.len < p0 + SR_CHUNK) ? en.start + en.len : p0 + SR_CHUNK;
     X acc = O::identity();
-    if (((uintptr_t)x & 15) == 0) {
+    if constexpr (OP == OP_AFFINE) {
+      // order-preserving: lane l folds the l-th contiguous 32nd of the chunk
+      // in order, the warp fold then composes the lanes in ascending order
+      const long long per = (p1 - p0 + 31) / 32;
+      const long long b = p0 + lane * per, e_ = (b + per < p1) ? b + per : p1;
+      for (long long p = b; p < e_; ++p) acc = O::combine(acc, E::make(__ldg(x + p)));
+    } else if (((uintptr_t)x & 15) == 0) {
       // granules g0 .. g1 round-robin over the lanes, 4 in flight per lane;
       // elements outside [p0, p1) are the identity
       constexpr int VEC = 16 / (int)sizeof(In);
@@ -325,20 +357,25 @@ __global__ void __launch_bounds__(SR_WARPS * 32) segrows_long(const __grid_const
 #pragma unroll
           for (int t = 0; t < VEC; ++t) {
             const long long q = (gb + 32 * u) * VEC + t;
-            if (gb + 32 * u < g1 && q >= p0 && q < p1) a4[u] = O::combine(a4[u], (X)e[u][t]);
+            if (gb + 32 * u < g1 && q >= p0 && q < p1) a4[u] = O::combine(a4[u], E::make(e[u][t]));
           }
         }
       }
       acc = O::combine(O::combine(a4[0], a4[1]), O::combine(a4[2], a4[3]));
     } else {
-      for (long long p = p0 + lane; p < p1; p += 32) acc = O::combine(acc, (X)__ldg(x + p));
+      for (long long p = p0 + lane; p < p1; p += 32) acc = O::combine(acc, E::make(__ldg(x + p)));
     }
     if constexpr (VERIFY) {
-      if (a.verify & V_COVERAGE)
-        for (long long q = p0 + lane; q < p1; q += 32) {
+      if (a.verify & V_COVERAGE) {
+        // the positions this lane folded (contiguous for the ordered op)
+        const long long per = OP == OP_AFFINE ? (p1 - p0 + 31) / 32 : 1;
+        const long long b = OP == OP_AFFINE ? p0 + lane * per : p0 + lane;
+        const long long e_ = OP == OP_AFFINE ? ((b + per < p1) ? b + per : p1) : p1;
+        for (long long q = b; q < e_; q += OP == OP_AFFINE ? 1 : 32) {
           a.owner[q] = leaf;
           atomicAdd(&a.count[q], 1u);
         }
+      }
     }
     acc = warp_fold<OP>(acc);
     const long long nchr = (en.len + SR_CHUNK - 1) / SR_CHUNK;
@@ -366,7 +403,7 @@ __global__ void __launch_bounds__(SR_WARPS * 32) segrows_long(const __grid_const
 template <typename In, int OP, int LPL, bool V>
 cudaError_t launch_blocks(const NestArgs& a, const SegRowsWS& ws, int grid, cudaStream_t s) {
   auto kern = segrows_blocks<In, OP, LPL, V>;
-  const size_t smem = (size_t)SR_WARPS * ((SR_RB + 1) * 8 + 32 * (LPL + 1) * 8);
+  const size_t smem = (size_t)SR_WARPS * ((SR_RB + 1) * 8 + 32 * (LPL + 1) * sizeof(SrFold<In, OP>));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, SR_WARPS * 32, smem, s>>>(a, ws);
@@ -388,6 +425,10 @@ cudaError_t launch_op(const NestArgs& a, const SegRowsWS& ws, int lpl, int ga, i
     case OP_SUM: return v ? launch_t<In, OP_SUM, true>(a, ws, lpl, ga, gb, s) : launch_t<In, OP_SUM, false>(a, ws, lpl, ga, gb, s);
     case OP_MIN: return v ? launch_t<In, OP_MIN, true>(a, ws, lpl, ga, gb, s) : launch_t<In, OP_MIN, false>(a, ws, lpl, ga, gb, s);
     case OP_MAX: return v ? launch_t<In, OP_MAX, true>(a, ws, lpl, ga, gb, s) : launch_t<In, OP_MAX, false>(a, ws, lpl, ga, gb, s);
+    case OP_AFFINE:
+      if constexpr (std::is_same<In, long long>::value)
+        return v ? launch_t<In, OP_AFFINE, true>(a, ws, lpl, ga, gb, s) : launch_t<In, OP_AFFINE, false>(a, ws, lpl, ga, gb, s);
+      return cudaErrorInvalidValue;
     default: return cudaErrorInvalidValue;
   }
 }
@@ -399,12 +440,16 @@ int64_t sr_cap_chunks(int64_t nnz) { return nnz / SR_CHUNK + nnz / SR_LONG + 64;
 
 // workspace bytes for nnz nonzeros (header, entries, chunk map, partials, tickets)
 size_t segrows_ws_bytes(int64_t nnz) {
-  return 64 + (size_t)sr_cap_ent(nnz) * (sizeof(SREntry) + 4) + (size_t)sr_cap_chunks(nnz) * (4 + 8) + 256;
+  return 64 + (size_t)sr_cap_ent(nnz) * (sizeof(SREntry) + 4) + (size_t)sr_cap_chunks(nnz) * (4 + 16) + 256;
 }
 
 bool segrows_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 2 || !a.keyed || !a.offsets) { *why = "not a keyed CSR nest"; return false; }
-  if (a.op != OP_SUM && a.op != OP_MIN && a.op != OP_MAX) { *why = "CSR rows: sum / min / max"; return false; }
+  if (a.op != OP_SUM && a.op != OP_MIN && a.op != OP_MAX && a.op != OP_AFFINE) {
+    *why = "CSR rows: sum / min / max / affine";
+    return false;
+  }
+  if (a.op == OP_AFFINE && a.in_dtype != DT_I64) { *why = "affine: int64 input"; return false; }
   if (a.in_dtype != DT_F32 && a.in_dtype != DT_F64 && a.in_dtype != DT_I32 && a.in_dtype != DT_I64) {
     *why = "CSR rows: dtype";
     return false;
@@ -440,7 +485,7 @@ cudaError_t launch_segrows(const NestArgs& a, void* wsbuf, int64_t ws_nnz, cudaS
   ws.ent = (SREntry*)p;
   p += ws.cap_ent * sizeof(SREntry);
   ws.part = p;
-  p += ws.cap_chunks * 8;
+  p += ws.cap_chunks * 16;  // up to the 16-byte affine pair
   ws.done = (unsigned*)p;
   p += ws.cap_ent * 4;
   ws.cmap = (int*)p;

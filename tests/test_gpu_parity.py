@@ -637,7 +637,7 @@ def test_segmented_misaligned_values(H, torch_mod, oracle, case, mis):
 
 
 @pytest.mark.parametrize("dt,op", [("f32", "min"), ("f32", "max"), ("f64", "sum"), ("f64", "min"), ("i32", "sum"),
-                                   ("i64", "sum"), ("i64", "max")])
+                                   ("i64", "sum"), ("i64", "max"), ("i64", "affine")])
 @pytest.mark.parametrize("case", ["zipf", "all_empty", "one_huge_row", "edges", "short_only", "unaligned_tail"])
 def test_segrows_ops_and_dtypes(H, torch_mod, oracle, case, dt, op):
     """The collapsed CSR nest (c3_fast_nest) for the ops and dtypes the fp32
@@ -658,28 +658,37 @@ def test_segrows_ops_and_dtypes(H, torch_mod, oracle, case, dt, op):
         v = rng.integers(-(1 << 31), (1 << 31) - 1, nnz, dtype=np.int64).astype(np.int32)
     else:
         v = rng.integers(-(1 << 62), 1 << 62, nnz, dtype=np.int64)
-    hop = {"sum": H.OP_SUM, "min": H.OP_MIN, "max": H.OP_MAX}[op]
+    hop = {"sum": H.OP_SUM, "min": H.OP_MIN, "max": H.OP_MAX, "affine": H.OP_AFFINE}[op]
     fp = dt in ("f32", "f64")
     for lpl in (16, 8):
         nest = H.Nest(nests.c3_fast_nest(lane_chunk=lpl), device=0, cluster_dim=2, warps_per_cta=8, clusters=5)
         xd = torch.from_numpy(v).cuda() if nnz else torch.zeros(4, dtype=torch.from_numpy(v).dtype, device="cuda")
         offd = torch.from_numpy(off).cuda()
-        out = torch.full((max(rows, 1),), -1, dtype=torch.float64 if fp else torch.int64, device="cuda")
+        shape = (max(rows, 1), 2) if op == "affine" else (max(rows, 1),)
+        out = torch.full(shape, -1, dtype=torch.float64 if fp else torch.int64, device="cuda")
         owner = torch.full((max(nnz, 1),), -1, dtype=torch.int64, device="cuda")
         count = torch.zeros(max(nnz, 1), dtype=torch.int32, device="cuda")
         for verify in (0, H.VERIFY_COVERAGE):
             out.fill_(-1)
             d = H.make_desc(xd, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd, op=hop,
-                            out_dtype=H.F64 if fp else H.I64, verify=verify,
+                            out_dtype=H.F64 if fp else (H.U64 if op == "affine" else H.I64), verify=verify,
                             owner=owner if verify else None, count=count if verify else None)
             nest.parallel_for_reduce(d)
             torch.cuda.synchronize()
             assert nest.last_kernel() == "segrows_csr"
             ref_levels = nests.c3_nest(with_gpu=False, rows_chunk=16, width=8)
-            o = oracle.nest_run(oracle_levels(oracle, ref_levels, 1, 2, 2, 4), n0=rows, offsets=off, x=v, op=hop,
+            o = None if op == "affine" else oracle.nest_run(oracle_levels(oracle, ref_levels, 1, 2, 2, 4), n0=rows, offsets=off, x=v, op=hop,
                                 keyed=True, coverage=False, partials=False)
             got = out.cpu().numpy()[:rows]
-            if fp and op == "sum":
+            if op == "affine":
+                # DESIGN reading #28: per row, the sequential composition (the
+                # direct recurrence); (A, B) pinned by y0 = 0 -> B, y0 = 1 -> A + B
+                g = got.view(np.uint64)
+                for r in range(rows):
+                    xr = v[off[r]:off[r + 1]]
+                    B = oracle.affine_run(xr, 0)
+                    assert int(g[r, 1]) == B and (int(g[r, 0]) + B) % (1 << 64) == oracle.affine_run(xr, 1), (case, r)
+            elif fp and op == "sum":
                 assert_rel(got, o.result)
             else:
                 assert np.array_equal(got, o.result), (case, dt, op)
