@@ -1001,6 +1001,43 @@ def test_segmented_nest_reuse_shrinking_nnz(H, torch_mod, oracle):
         assert_rel(out.cpu().numpy(), oracle.segsum_f32(v, off))
 
 
+def test_segrows_nest_reuse_shrinking_nnz(H, torch_mod, oracle):
+    """The CSR rows kernel's workspace keeps the layout of its capacity too:
+    one Nest, fp64 sums over a large CSR with long rows, smaller ones, and
+    the large one again, interleaved with an int64 MAX call (another
+    instantiation on the same workspace); every call vs the oracle."""
+    from paper_2309_01906_b200 import nests
+    from tests.nestutil import oracle_levels
+    torch = torch_mod
+    rng = np.random.default_rng(4243)
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=6)
+    ol = oracle_levels(oracle, nests.c3_nest(with_gpu=False, rows_chunk=16, width=8), 1, 2, 2, 4)
+
+    def case(rows, p_long):
+        lens = np.where(rng.random(rows) < p_long, rng.integers(4097, 60000, rows), rng.geometric(0.1, rows))
+        return np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+
+    offs = [case(4000, 0.02), case(600, 0.05), case(50, 0.2), case(4000, 0.02)]
+    for k, off in enumerate(offs + offs[::-1]):
+        rows, nnz = off.size - 1, int(off[-1])
+        if k % 2 == 0:
+            v, op, odt, tdt = rng.standard_normal(nnz), H.OP_SUM, H.F64, torch.float64
+        else:
+            v, op, odt, tdt = rng.integers(-(1 << 40), 1 << 40, nnz, dtype=np.int64), H.OP_MAX, H.I64, torch.int64
+        out = torch.full((rows,), -1, dtype=tdt, device="cuda")
+        d = H.make_desc(torch.from_numpy(v).cuda(), out, n0=rows, n1=nnz, nloops=2, keyed=True, op=op,
+                        offsets=torch.from_numpy(off).cuda(), out_dtype=odt)
+        nest.parallel_for_reduce(d)
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "segrows_csr"
+        want = oracle.nest_run(ol, n0=rows, offsets=off, x=v, op=op, keyed=True, coverage=False,
+                               partials=False).result
+        if op == H.OP_SUM:
+            assert_rel(out.cpu().numpy(), want)
+        else:
+            assert np.array_equal(out.cpu().numpy(), want)
+
+
 def test_segmented_empty_caller_shard(H, torch_mod):
     """A caller-sharded CSR rank with no rows (local_n0 = 0 ->
     HPAR_LOCAL_N0_EMPTY) returns without a launch and writes nothing (ADVICE
