@@ -12,7 +12,8 @@ times (same nests, geometry and kernels):
       the oracle's numpy steps over the whole array
 Edge cases at their stated sizes: C4 with 2^32 equal bytes (bin 0 = 2^32,
 beyond any u32 counter), C3 with one row of 2^26 nonzeros between empty rows,
-C3 past 2^31 nonzeros per rank (sampled rows around position 2^31).
+C3 past 2^31 nonzeros per rank (sampled rows around position 2^31), C2 with
+ragged rows (4095 columns) and C3 with fp64 values (the CSR rows kernel).
 The oracle runs range by range in a process pool (tests/fullsize_oracle.py:
 every quantity is exact and additive over disjoint ranges).
 Inputs come from the device generator, which is cross-checked bit for bit
@@ -297,3 +298,43 @@ def test_c3_beyond_2e31_nonzeros(env, oracle):
         assert_rel(got[r:r + 1], want)
     exact = F.exact_numerator_sum(gen.SEED_C3, nnz) * 2.0 ** -24
     assert abs(got.sum() - exact) <= 1e-9 * exact
+
+
+def test_c2_full_ragged_rows(env, oracle):
+    """C2's matrix with ragged rows at full size: 65536 x 4095 at ld 4095
+    (every row starts at a different offset inside a 16-byte granule) on the
+    fused row-wise kernel in bench.py's geometry; every row vs the oracle."""
+    torch, H, nests, L = env
+    K, W, C = bench_geometry("c2")
+    rows, cols = 65536, 4095
+    nest = H.Nest(nests.c2_nest(), device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+    x = torch.empty(rows * cols, dtype=torch.float32, device="cuda")
+    L.hpar_inputs_fill_f32(gen.SEED_C2, 0, rows * cols, x.data_ptr(), None)
+    out = torch.empty(rows, dtype=torch.float32, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=rows, n1=cols, ld=cols, nloops=2, keyed=True))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "rowwise_tma_dsmem"
+    assert_rel(out.cpu().numpy(), oracle.rowsum_f32(gen.gen_f32(gen.SEED_C2, 0, rows * cols), rows, cols))
+
+
+def test_c3_full_fp64_values(env, oracle):
+    """C3's matrix (2^24 rows, 2^28 nonzeros, the longest row 1.8e7) with
+    fp64 values on the CSR rows kernel: the values are the fp32 inputs
+    widened exactly, so every row vs the oracle's fp64 segment sums of the
+    same numbers; a second call checks the self-resetting chunk tickets."""
+    torch, H, nests, L = env
+    rows, nnz = 1 << 24, 1 << 28
+    off = gen.csr_offsets(rows, nnz)
+    v32 = gen.gen_f32(gen.SEED_C3, 0, nnz)
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8)
+    x = torch.from_numpy(v32).cuda().double()
+    offd = torch.from_numpy(off).cuda()
+    out = torch.empty(rows, dtype=torch.float64, device="cuda")
+    want = oracle.segsum_f32(v32, off)
+    for _ in range(2):
+        out.fill_(-1.0)
+        nest.parallel_for_reduce(H.make_desc(x, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd,
+                                             out_dtype=H.F64))
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "segrows_csr"
+        assert_rel(out.cpu().numpy(), want)
