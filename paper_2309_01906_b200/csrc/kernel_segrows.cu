@@ -40,6 +40,9 @@ constexpr int SR_WARPS = 8;         // warps per CTA (the nest's W)
 #ifndef SR_MINB
 #define SR_MINB 3                   // min resident CTAs (register budget: 80; 1 and 4 measured slower)
 #endif
+#ifndef SR_PF_L2
+#define SR_PF_L2 0                  // prefetch into L2 instead of L1 (A/B knob)
+#endif
 #ifndef SR_PF
 #define SR_PF 2                     // windows ahead the lanes prefetch into L1
 #endif
@@ -215,7 +218,13 @@ __global__ void __launch_bounds__(SR_WARPS * 32, SR_MINB) segrows_blocks(const _
             if (q0 < we) gran_elems<In>(__ldg((const int4*)x + q0 / VEC), e);  // a granule holding a valid element
             // a later window's line of this lane into L1, in flight while
             // this window is reduced (one prefetch per lane covers its run)
-            if (g == 0 && q0 + SR_PF * WIN < P1) asm volatile("prefetch.global.L1 [%0];" ::"l"(x + q0 + SR_PF * WIN));
+            if (g == 0 && q0 + SR_PF * WIN < P1) {
+#if SR_PF_L2
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(x + q0 + SR_PF * WIN));
+#else
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(x + q0 + SR_PF * WIN));
+#endif
+            }
 #pragma unroll
             for (int t = 0; t < VEC; ++t) {
               const long long q = q0 + t;
