@@ -13,7 +13,8 @@ times (same nests, geometry and kernels):
 Edge cases at their stated sizes: C4 with 2^32 equal bytes (bin 0 = 2^32,
 beyond any u32 counter), C3 with one row of 2^26 nonzeros between empty rows,
 C3 past 2^31 nonzeros per rank (sampled rows around position 2^31), C2 with
-ragged rows (4095 columns) and C3 with fp64 values (the CSR rows kernel).
+ragged rows (4095 columns) and C3 with fp64 values (the CSR rows kernel);
+C3's coverage at full size (every one of 2^28 nonzeros visited once).
 The oracle runs range by range in a process pool (tests/fullsize_oracle.py:
 every quantity is exact and additive over disjoint ranges).
 Inputs come from the device generator, which is cross-checked bit for bit
@@ -338,3 +339,35 @@ def test_c3_full_fp64_values(env, oracle):
         torch.cuda.synchronize()
         assert nest.last_kernel() == "segrows_csr"
         assert_rel(out.cpu().numpy(), want)
+
+
+def test_c3_full_coverage(env):
+    """C3 at full size with the coverage outputs (§8(c) "no loss, no
+    duplication" at 2^28 iterations): every nonzero visited exactly once,
+    owners valid leaf ids, and each sampled block's short rows on one warp
+    (the dynamic(256) row blocks are warp tasks; reading #14)."""
+    torch, H, nests, L = env
+    rows, nnz = 1 << 24, 1 << 28
+    off = gen.csr_offsets(rows, nnz)
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8)
+    x = torch.empty(nnz, dtype=torch.float32, device="cuda")
+    L.hpar_inputs_fill_f32(gen.SEED_C3, 0, nnz, x.data_ptr(), None)
+    offd = torch.from_numpy(off).cuda()
+    out = torch.empty(rows, dtype=torch.float32, device="cuda")
+    owner = torch.full((nnz,), -1, dtype=torch.int64, device="cuda")
+    count = torch.zeros(nnz, dtype=torch.int32, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd,
+                                         verify=H.VERIFY_COVERAGE, owner=owner, count=count))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "segmented_csr"
+    assert int((count != 1).sum().item()) == 0, "a nonzero visited zero or several times"
+    threads = int(nest.info().threads_per_gpu)
+    own = owner.cpu().numpy()
+    assert own.min() >= 0 and own.max() < threads
+    lens = np.diff(off)
+    rng = np.random.default_rng(8)
+    for b0 in rng.integers(0, rows // 256, 400) * 256:
+        rs = [r for r in range(b0, b0 + 256) if 0 < lens[r] <= 4096]
+        if rs:
+            w = np.concatenate([own[off[r]:off[r + 1]] for r in rs]) // 32
+            assert (w == w[0]).all(), f"block {b0}: short rows on several warps"
