@@ -54,6 +54,9 @@
 namespace hpar {
 namespace {
 
+#ifndef SEG_ABL
+#define SEG_ABL 0  // timing ablations only (wrong results): 1 = no window prefix, 2 = no row steps
+#endif
 constexpr int RB = 256;            // rows per block claim
 constexpr int64_t LONG = 4096;     // a row with more nonzeros is split (default; HPAR_SEG_LONG)
 constexpr int64_t SPLIT_MIN = 256;  // smallest split threshold the queue is sized for
@@ -702,7 +705,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
       const int emax = (int)(gmax >> 23), emin = (int)((gmin + 1u) >> 24);
 #endif
       const bool exact = emax < 255 && emax - emin <= EXACT_BINADES;
-      if (exact) {
+      if (exact && !(SEG_ABL & 1)) {
         // lane-local prefix at even positions: pair sums, then their prefix
         // in two independent halves (short dependency chains)
         double c[LPL / 2];  // c[j] = v[0] + ... + v[2j+1]
@@ -735,7 +738,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) segmented_kernel(const __gri
       // past the window's rows compute a discarded value instead of branching.
       const bool tail_win = wend > lim4;  // the array's unaligned tail is not in the ring
       int r = rcur;
-      for (;;) {
+      for (; !(SEG_ABL & 2);) {
         const int i = r + lane;
         const int s_ = sm.off[i < nr ? i : nr];
         const int e_ = sm.off[i + 1 < nr ? i + 1 : nr];
