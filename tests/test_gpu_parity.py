@@ -936,6 +936,106 @@ def test_segmented_fuzz(H, torch_mod, oracle, seed):
         assert (count.cpu().numpy()[:nnz] == 1).all()
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_segrows_fuzz(H, torch_mod, oracle, seed):
+    """Random CSR shapes on the CSR rows kernel: empty / short / medium /
+    long (> 4096) rows in random order, a random op and dtype (MIN / MAX over
+    fp32; SUM / MIN / MAX over fp64, int32, int64; AFFINE over int64), a
+    random lane chunk, grid and value-pointer offset.  Every row vs the
+    oracle (the nest walk of the generic CSR nest; AFFINE per row against the
+    direct recurrence), every nonzero visited once."""
+    from paper_2309_01906_b200 import nests
+    from tests.nestutil import oracle_levels
+    torch = torch_mod
+    rng = np.random.default_rng(2000 + seed)
+    rows = int(rng.integers(1, 2500))
+    kind = rng.choice(4, size=rows, p=[0.3, 0.5, 0.17, 0.03])
+    lens = np.where(kind == 0, 0, np.where(kind == 1, rng.geometric(0.2, rows),
+                    np.where(kind == 2, rng.integers(30, 2500, rows), rng.integers(4097, 40000, rows))))
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(off[-1])
+    combos = [("f32", H.OP_MIN), ("f32", H.OP_MAX), ("f64", H.OP_SUM), ("f64", H.OP_MIN), ("f64", H.OP_MAX),
+              ("i32", H.OP_SUM), ("i32", H.OP_MIN), ("i64", H.OP_SUM), ("i64", H.OP_MAX), ("i64", H.OP_AFFINE)]
+    dt, op = combos[int(rng.integers(len(combos)))]
+    if dt == "f32":
+        v = (rng.standard_normal(nnz) * 10 ** rng.uniform(-3, 3)).astype(np.float32)
+    elif dt == "f64":
+        v = rng.standard_normal(nnz) + float(rng.uniform(-2, 2))
+    elif dt == "i32":
+        v = rng.integers(-(1 << 31), (1 << 31) - 1, nnz, dtype=np.int64).astype(np.int32)
+    else:
+        v = rng.integers(-(1 << 62), 1 << 62, nnz, dtype=np.int64)
+    lpl = int(rng.choice([8, 16]))
+    nest = H.Nest(nests.c3_fast_nest(lane_chunk=lpl), device=0, cluster_dim=2, warps_per_cta=8,
+                  clusters=int(rng.integers(1, 9)))
+    shift = int(rng.integers(0, 16 // v.itemsize))  # elements off a 16-byte granule
+    raw = torch.zeros(nnz + 16, dtype=torch.from_numpy(v[:0]).dtype, device="cuda")
+    xd = raw[shift:shift + nnz]
+    if nnz:
+        xd.copy_(torch.from_numpy(v).cuda())
+    offd = torch.from_numpy(off).cuda()
+    fp = dt in ("f32", "f64")
+    shape = (rows, 2) if op == H.OP_AFFINE else (rows,)
+    out = torch.full(shape, -1, dtype=torch.float64 if fp else torch.int64, device="cuda")
+    owner = torch.full((max(nnz, 1),), -1, dtype=torch.int64, device="cuda")
+    count = torch.zeros(max(nnz, 1), dtype=torch.int32, device="cuda")
+    odt = H.F64 if fp else (H.U64 if op == H.OP_AFFINE else H.I64)
+    d = H.make_desc(xd, out, n0=rows, n1=nnz, nloops=2, keyed=True, offsets=offd, op=op, out_dtype=odt,
+                    verify=H.VERIFY_COVERAGE, owner=owner, count=count)
+    nest.parallel_for_reduce(d)
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "segrows_csr"
+    got = out.cpu().numpy()
+    if op == H.OP_AFFINE:
+        g = got.view(np.uint64)
+        for r in range(rows):
+            xr = v[off[r]:off[r + 1]]
+            B = oracle.affine_run(xr, 0)
+            assert int(g[r, 1]) == B and (int(g[r, 0]) + B) % (1 << 64) == oracle.affine_run(xr, 1), r
+    else:
+        ol = oracle_levels(oracle, nests.c3_nest(with_gpu=False, rows_chunk=16, width=8), 1, 2, 2, 4)
+        want = oracle.nest_run(ol, n0=rows, offsets=off, x=v, op=op, keyed=True, coverage=False,
+                               partials=False).result
+        if fp and op == H.OP_SUM:
+            assert_rel(got, want)
+        else:
+            assert np.array_equal(got, want)
+    if nnz:
+        assert (count.cpu().numpy()[:nnz] == 1).all()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_rowwise_fuzz(H, torch_mod, oracle, seed):
+    """Random dense-row shapes on the fused row-wise kernel: rows, columns,
+    leading dimension, pointer offset, K, W, C, op and dtype at random
+    (ragged or aligned); rows, owner map and every level's partials vs the
+    oracle."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    rng = np.random.default_rng(3000 + seed)
+    n0 = int(rng.integers(1, 120))
+    n1 = int(rng.choice([int(rng.integers(1, 40)), int(rng.integers(40, 5000))]))
+    ld = n1 + int(rng.choice([0, 0, int(rng.integers(1, 9))]))
+    K, W = int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 8]))
+    C = int(rng.integers(1, 12))
+    combos = [("f32", H.OP_SUM), ("f32", H.OP_MIN), ("f64", H.OP_SUM), ("f64", H.OP_MAX), ("i32", H.OP_SUM),
+              ("i64", H.OP_MIN), ("i64", H.OP_AFFINE)]
+    dt, op = combos[int(rng.integers(len(combos)))]
+    if dt == "f32":
+        x = gen.gen_f32(gen.SEED_C2 + seed, 0, n0 * n1)
+    elif dt == "f64":
+        x = rng.standard_normal(n0 * n1)
+    elif dt == "i32":
+        x = rng.integers(-(1 << 31), (1 << 31) - 1, n0 * n1, dtype=np.int64).astype(np.int32)
+    else:
+        x = rng.integers(-(1 << 62), 1 << 62, n0 * n1, dtype=np.int64)
+    mis = int(rng.integers(0, 16 // x.itemsize)) * x.itemsize
+    levels = nests.c2_nest()
+    res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=True, op=op, C=C, K=K, W=W, ld=ld, misalign=mis)
+    assert res["kernel"] == "rowwise_tma_dsmem", (n0, n1, ld, K, W, dt, op)
+    compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, op=op, C=C, K=K, W=W)
+
+
 @pytest.mark.parametrize("values", ["zeros_normal", "zeros_tiny", "subnormal_only", "zero_rows"])
 def test_segmented_explicit_zeros(H, torch_mod, oracle, values):
     """Explicit zeros and subnormals in the CSR values (DESIGN reading on the
