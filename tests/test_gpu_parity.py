@@ -1005,6 +1005,39 @@ def test_segrows_fuzz(H, torch_mod, oracle, seed):
 
 
 @pytest.mark.parametrize("seed", range(12))
+def test_flat_fuzz(H, torch_mod, oracle, seed):
+    """Random flat shapes on the fused flat kernel: length (empty, ragged,
+    several tiles), tile, K, W, C, op, dtype (fp32 / int32 / fp64 / int64,
+    AFFINE over int64) and pointer offset at random; total, owner map and
+    every level's partials vs the oracle."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    rng = np.random.default_rng(4000 + seed)
+    K, W = int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 8]))
+    combos = [("f32", H.OP_SUM), ("f32", H.OP_MAX), ("i32", H.OP_SUM), ("i32", H.OP_MIN), ("f64", H.OP_SUM),
+              ("f64", H.OP_MIN), ("i64", H.OP_SUM), ("i64", H.OP_AFFINE)]
+    dt, op = combos[int(rng.integers(len(combos)))]
+    esz = 8 if dt in ("f64", "i64") else 4
+    tile = 128 * W * int(rng.choice([1, 2, 4, 8]))
+    tile = min(tile, 32768 // esz) // (128 * W) * (128 * W) or 128 * W
+    C = int(rng.integers(1, 10))
+    n = int(rng.choice([0, int(rng.integers(1, 3000)), int(rng.integers(3000, 400000))]))
+    if dt == "f32":
+        x = gen.gen_f32(gen.SEED_C5 + seed, 0, n)
+    elif dt == "i32":
+        x = gen.gen_i32(gen.SEED_C1 + seed, 0, n)
+    elif dt == "f64":
+        x = rng.standard_normal(n) + 1.0
+    else:
+        x = rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)
+    mis = int(rng.integers(0, 16 // esz)) * esz if n else 0
+    levels = nests.flat_nest(K=K, tile=tile, vec=4)
+    res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis)
+    assert res["kernel"] == "flat_tma", (n, tile, K, W, dt)
+    compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
+
+
+@pytest.mark.parametrize("seed", range(12))
 def test_rowwise_fuzz(H, torch_mod, oracle, seed):
     """Random dense-row shapes on the fused row-wise kernel: rows, columns,
     leading dimension, pointer offset, K, W, C, op and dtype at random
