@@ -1038,6 +1038,30 @@ def test_flat_fuzz(H, torch_mod, oracle, seed):
 
 
 @pytest.mark.parametrize("seed", range(12))
+def test_hist_fuzz(H, torch_mod, oracle, seed):
+    """Random shapes on the histogram kernel: length, tile, K, W (private or
+    shared lane-table regions), C, pointer offset, uniform / skewed / constant
+    bytes; bins, owner map and every level's partials vs the oracle."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    rng = np.random.default_rng(5000 + seed)
+    K, W = int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 6, 8]))
+    tile = 512 * W * int(rng.choice([1, 2, 4]))
+    tile = min(tile, 32768) // (512 * W) * (512 * W) or 512 * W
+    C = int(rng.integers(1, 8))
+    n = int(rng.choice([0, int(rng.integers(1, 5000)), int(rng.integers(5000, 300000))]))
+    kind = int(rng.integers(3))
+    x = (gen.gen_u8(gen.SEED_C4 + seed, 0, n) if kind == 0 else gen.gen_u8_zipf(gen.SEED_C4 + seed, 0, n)
+         if kind == 1 else np.full(n, int(rng.integers(256)), dtype=np.uint8))
+    mis = int(rng.integers(0, 16)) if n else 0
+    levels = nests.c4_nest(K=K, tile=tile)
+    res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, misalign=mis)
+    assert res["kernel"].startswith("hist256_lanepriv"), (n, tile, K, W)
+    assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
+    compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
+
+
+@pytest.mark.parametrize("seed", range(12))
 def test_rowwise_fuzz(H, torch_mod, oracle, seed):
     """Random dense-row shapes on the fused row-wise kernel: rows, columns,
     leading dimension, pointer offset, K, W, C, op and dtype at random
