@@ -175,6 +175,10 @@ __global__ void __launch_bounds__(SR_WARPS * 32, SR_MINB) segrows_blocks(const _
         const unsigned long long nch = (unsigned long long)((len + SR_CHUNK - 1) / SR_CHUNK);
         const unsigned long long old = atomicAdd(&ws.hdr[1], (1ull << 40) + nch);
         const long long e = (long long)(old >> 40), cb = (long long)(old & ((1ull << 40) - 1));
+        // capacity by construction: every entry holds > SR_LONG nonzeros and
+        // every chunk >= 1, so entries <= nnz / SR_LONG and chunks <= nnz /
+        // SR_CHUNK + entries, both below the workspace's caps (the guard only
+        // keeps a corrupted offsets array from writing out of bounds)
         if (e < ws.cap_ent && cb + (long long)nch <= ws.cap_chunks) {
           ws.ent[e] = SREntry{r0 + i, off[i], len, cb};
           for (unsigned long long j = 0; j < nch; ++j) ws.cmap[cb + j] = (int)e;
