@@ -194,3 +194,19 @@ def test_affine_ordered_fold(oracle):
             for pidx in range(kids.shape[0]):
                 assert _compose(kids[pidx]) == tuple(int(v) for v in r.partials[a - 1][pidx])
     assert oracle.affine_run(x[::-1].copy(), 3) != oracle.affine_run(x, 3)
+
+
+def test_affine_run_pinned_to_python_recurrence(oracle):
+    """or_affine_run against the recurrence written out in Python integers
+    (S:377's ordered fold of the element maps y -> (2x+1) y + x^2, mod 2^64),
+    including negative int64 inputs (two's complement) and the empty run."""
+    M = 1 << 64
+    rng = np.random.default_rng(7)
+    for n in (0, 1, 2, 17, 300):
+        x = rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)
+        for y0 in (0, 1, 3, M - 1):
+            y = y0
+            for v in x.tolist():
+                u = v % M
+                y = ((2 * u + 1) * y + u * u) % M
+            assert oracle.affine_run(x, y0) == y
