@@ -7,7 +7,7 @@
 //     cluster..warp        dynamic(256)    loop 0: blocks of 256 rows claimed by warps
 //     lane                 static(LPL)     loop 2: the block's collapsed (row, nonzero) list
 // Rows longer than 4096 nonzeros are re-bound by length class to
-// dynamic(16384) chunks over all warps of the grid (P:244-253 chunking).
+// dynamic(4096) chunks over all warps of the grid (P:244-253 chunking).
 //
 // B200 design: no exact-prefix trick exists for MIN/MAX or for fp64 values,
 // so a window of 32·LPL positions is reduced as a segmented reduction:
@@ -35,7 +35,10 @@ namespace {
 
 constexpr int SR_RB = 256;          // rows per block claim (the nest's dynamic(256))
 constexpr int64_t SR_LONG = 4096;   // longer rows are chunked over the grid
-constexpr int64_t SR_CHUNK = 16384; // positions per long-row chunk
+#ifndef SR_CHUNK_LEN
+#define SR_CHUNK_LEN 4096  // 4096: -1.5% vs 16384 (8192 between; scripts/segrows_ab.sh)
+#endif
+constexpr int64_t SR_CHUNK = SR_CHUNK_LEN;  // positions per long-row chunk
 constexpr int SR_WARPS = 8;         // warps per CTA (the nest's W)
 #ifndef SR_MINB
 #define SR_MINB 3                   // min resident CTAs (register budget: 80; 1 and 4 measured slower)
