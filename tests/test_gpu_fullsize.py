@@ -14,7 +14,8 @@ Edge cases at their stated sizes: C4 with 2^32 equal bytes (bin 0 = 2^32,
 beyond any u32 counter), C3 with one row of 2^26 nonzeros between empty rows,
 C3 past 2^31 nonzeros per rank (sampled rows around position 2^31), C2 with
 ragged rows (4095 columns) and C3 with fp64 values (the CSR rows kernel);
-C3's coverage at full size (every one of 2^28 nonzeros visited once).
+C3's coverage at full size (every one of 2^28 nonzeros visited once); the
+8-byte flat path past 4 GiB of input (fp64 and int64, exact totals).
 The oracle runs range by range in a process pool (tests/fullsize_oracle.py:
 every quantity is exact and additive over disjoint ranges).
 Inputs come from the device generator, which is cross-checked bit for bit
@@ -371,3 +372,36 @@ def test_c3_full_coverage(env):
         if rs:
             w = np.concatenate([own[off[r]:off[r + 1]] for r in rs]) // 32
             assert (w == w[0]).all(), f"block {b0}: short rows on several warps"
+
+
+def test_flat_fp64_and_int64_past_4gib(env, oracle):
+    """The 8-byte flat path past 32-bit BYTE offsets: 2^30 + 12345 fp64
+    (8.6 GB) — C5's fp32 inputs widened exactly, so the oracle's exact
+    Σk 2^-24 is the total — and the same count of int64 (their numerators
+    k), whose sum is exact; bench.py's C5 geometry; also 8 bytes off a
+    granule."""
+    from tests import fullsize_oracle as F
+    torch, H, nests, L = env
+    K, W, C = bench_geometry("c5")
+    n = (1 << 30) + 12345
+    nest = H.Nest(nests.c5_nest(K), device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+    x32 = torch.empty(n, dtype=torch.float32, device="cuda")
+    L.hpar_inputs_fill_f32(gen.SEED_C5, 0, n, x32.data_ptr(), None)
+    ksum = F.exact_numerator_sum(gen.SEED_C5, n)
+    raw = torch.empty(n + 2, dtype=torch.float64, device="cuda")
+    for off in (0, 1):
+        x = raw[off:off + n]
+        x.copy_(x32)
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        nest.parallel_for_reduce(H.make_desc(x, out, n0=n))
+        torch.cuda.synchronize()
+        assert nest.last_kernel() == "flat_tma"
+        assert_rel(out.cpu().numpy(), np.array([ksum * 2.0 ** -24]), tol=1e-12)
+    del raw
+    xi = (x32.double() * float(1 << 24)).long()
+    del x32
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(xi, out, n0=n))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "flat_tma"
+    assert int(out.item()) == ksum
