@@ -15,7 +15,8 @@ beyond any u32 counter), C3 with one row of 2^26 nonzeros between empty rows,
 C3 past 2^31 nonzeros per rank (sampled rows around position 2^31), C2 with
 ragged rows (4095 columns) and C3 with fp64 values (the CSR rows kernel);
 C3's coverage at full size (every one of 2^28 nonzeros visited once); the
-8-byte flat path past 4 GiB of input (fp64 and int64, exact totals).
+8-byte flat path past 4 GiB of input (fp64 and int64, exact totals) and the
+row-wise fp64 path past 4 GiB (rows equal to the oracle's exact sums).
 The oracle runs range by range in a process pool (tests/fullsize_oracle.py:
 every quantity is exact and additive over disjoint ranges).
 Inputs come from the device generator, which is cross-checked bit for bit
@@ -405,3 +406,24 @@ def test_flat_fp64_and_int64_past_4gib(env, oracle):
     torch.cuda.synchronize()
     assert nest.last_kernel() == "flat_tma"
     assert int(out.item()) == ksum
+
+
+def test_rowwise_fp64_past_4gib(env, oracle):
+    """The row-wise kernel's 64-bit partial path past 4 GiB of input:
+    150000 x 4096 fp64 rows (4.9 GB) holding C2's fp32 values widened
+    exactly; every row sum is exact in fp64 (36 significant bits), so the
+    rows must EQUAL the oracle's fp64 row sums of the same numbers."""
+    torch, H, nests, L = env
+    K, W, C = bench_geometry("c2")
+    rows, cols = 150000, 4096
+    nest = H.Nest(nests.c2_nest(), device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+    x32 = torch.empty(rows * cols, dtype=torch.float32, device="cuda")
+    L.hpar_inputs_fill_f32(gen.SEED_C2, 0, rows * cols, x32.data_ptr(), None)
+    x = x32.double()
+    del x32
+    out = torch.empty(rows, dtype=torch.float64, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=rows, n1=cols, ld=cols, nloops=2, keyed=True, out_dtype=H.F64))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "rowwise_tma_dsmem"
+    want = oracle.rowsum_f32(gen.gen_f32(gen.SEED_C2, 0, rows * cols), rows, cols)
+    assert np.array_equal(out.cpu().numpy(), want)
