@@ -17,6 +17,10 @@
 // (fp32 pairwise inside a vector, fp64 across vectors: §8(c) reading #6).
 // The lane -> warp -> CTA -> cluster -> GPU combine runs once at the end
 // (fused_common.cuh).  No GPU-scope fence inside the stream loop.
+// Also served: fp32 / int32 / fp64 / int64 inputs with SUM / MIN / MAX, the
+// ordered AFFINE op over int64 (every fold ascends, so the result is the
+// nest's fold), and inputs 4 / 8 / 12 bytes off a 16-byte granule (MIS: the
+// ring takes each tile's enclosing granules; lanes shift by the offset).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <type_traits>
