@@ -307,8 +307,12 @@ hpar_status hpar_shard_range_csr(const int64_t* offsets, int64_t rows, int32_t n
 /* §8(a) A2-A9: execute the nest over the loop(s) in `desc` and reduce.
  * One launch of a kernel specialisation picked by the planner (the generic
  * nest interpreter, or a fused streaming kernel when the nest matches its
- * shape), followed on the same stream by one ncclAllReduce at the node level
- * when the GPU level has more than one rank (total mode).  Errors:
+ * shape: flat, teams x threads, row-wise, histogram, CSR fp32 sums, CSR
+ * other ops / dtypes — hpar_last_kernel names it), followed on the same
+ * stream by one ncclAllReduce at the node level when the GPU level has more
+ * than one rank (total mode; ordered ops: allgather + rank-order fold).  A
+ * CSR call at >= 2^31 nonzeros per rank without a proving max_inner first
+ * measures its row-block spans (one host synchronisation).  Errors:
  * HPAR_E_INVALID (pointers, sizes, alignment of verify buffers),
  * HPAR_E_SCHEDULE (schedule NONE overflow), HPAR_E_UNSUPPORTED (op/dtype),
  * HPAR_E_CAPABILITY (keyed results whose combine would need a barrier the
