@@ -16,7 +16,8 @@ C3 past 2^31 nonzeros per rank (sampled rows around position 2^31), C2 with
 ragged rows (4095 columns) and C3 with fp64 values (the CSR rows kernel);
 C3's coverage at full size (every one of 2^28 nonzeros visited once); the
 8-byte flat path past 4 GiB of input (fp64 and int64, exact totals) and the
-row-wise fp64 path past 4 GiB (rows equal to the oracle's exact sums).
+row-wise fp64 path past 4 GiB (rows equal to the oracle's exact sums); the CSR
+rows kernel past 2^31 nonzeros (int32 sums, sampled rows).
 The oracle runs range by range in a process pool (tests/fullsize_oracle.py:
 every quantity is exact and additive over disjoint ranges).
 Inputs come from the device generator, which is cross-checked bit for bit
@@ -427,3 +428,35 @@ def test_rowwise_fp64_past_4gib(env, oracle):
     assert nest.last_kernel() == "rowwise_tma_dsmem"
     want = oracle.rowsum_f32(gen.gen_f32(gen.SEED_C2, 0, rows * cols), rows, cols)
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_segrows_beyond_2e31_nonzeros(env, oracle):
+    """The CSR rows kernel past 2^31 nonzeros (its positions are 64-bit
+    outside a window): 2^23 zipf rows over 2^31 + 12345 int32 values, SUM
+    into int64 rows (exact).  Sampled rows — around position 2^31, the
+    longest, the last, random ones — vs the oracle's nest walk of each row."""
+    from tests.nestutil import oracle_levels
+    torch, H, nests, L = env
+    rows, nnz = 1 << 23, (1 << 31) + 12345
+    off = gen.csr_offsets(rows, nnz)
+    lens = np.diff(off)
+    x = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    L.hpar_inputs_fill_i32(gen.SEED_C1, 0, nnz, x.data_ptr(), None)
+    out = torch.full((rows,), -1, dtype=torch.int64, device="cuda")
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8)
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=rows, n1=nnz, nloops=2, keyed=True,
+                                         offsets=torch.from_numpy(off).cuda(), out_dtype=H.I64))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "segrows_csr"
+    got = out.cpu().numpy()
+    ol = oracle_levels(oracle, nests.c3_nest(with_gpu=False, rows_chunk=16, width=8), 1, 1, 1, 1)
+    r31 = int(np.searchsorted(off, 1 << 31, side="right")) - 1
+    rng = np.random.default_rng(6)
+    sample = set(range(max(0, r31 - 200), min(rows, r31 + 200))) | set(range(rows - 200, rows))
+    sample |= set(np.argsort(lens)[-4:].tolist()) | set(rng.integers(0, rows, 300).tolist())
+    for r in sorted(sample):
+        b, n = int(off[r]), int(lens[r])
+        v = gen.gen_i32(gen.SEED_C1, b, n)
+        want = oracle.nest_run(ol, n0=1, offsets=np.array([0, n], dtype=np.int64), x=v, keyed=True,
+                               coverage=False, partials=False).result
+        assert int(got[r]) == int(want[0]), r
