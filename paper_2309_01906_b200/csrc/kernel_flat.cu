@@ -37,7 +37,7 @@ __host__ __device__ __forceinline__ uint32_t stage_stride(uint32_t tile_bytes, b
   return mis ? tile_bytes + 16 : tile_bytes;
 }
 
-template <typename In, typename Acc, int OP, bool VERIFY, bool MIS>
+template <typename In, typename Acc, int OP, bool VERIFY, bool MIS, int V = 4>
 __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant__ NestArgs a, int W,
                                                             int tile) {
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
     }
   } else {
     // ---------------- W consumer warps ----------------------------------
-    const int vec_per_tile = tile / 4;
+    const int vec_per_tile = tile / V;  // lane chunks of V elements
     const int64_t leaf = (int64_t)a.rank * a.threads_per_gpu + b * W * 32 + threadIdx.x;
     unsigned long long fpo = 0, fpw = 0, fpn = 0;
     for (int64_t j = 0; j < my_tiles; ++j) {
@@ -99,7 +99,37 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
       mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
       const In* st = (const In*)(dsm + (size_t)s * stride + mis);
       if (len == tile) {
-        if constexpr (sizeof(In) == 4 && MIS) {
+        if constexpr (V != 4) {
+          // lane static(1) / static(2): scalar shared loads of the lane's
+          // chunk (fp32 sums pairwise inside a chunk, fp64 across)
+#pragma unroll 4
+          for (int f = warp * 32 + lane; f < vec_per_tile; f += W * 32) {
+            In e[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) e[q] = st[V * f + q];
+            if constexpr (OP == OP_SUM && std::is_same<In, float>::value) {
+              float ps = e[0];
+#pragma unroll
+              for (int q = 1; q < V; ++q) ps += e[q];
+              acc += (double)ps;
+            } else {
+              Acc c = ElemT<OP, Acc, In>::make(e[0]);
+#pragma unroll
+              for (int q = 1; q < V; ++q) c = OpT<OP, Acc>::combine(c, ElemT<OP, Acc, In>::make(e[q]));
+              acc = OpT<OP, Acc>::combine(acc, c);
+            }
+            if constexpr (VERIFY) {
+              for (int q = 0; q < V; ++q) {
+                const int64_t it = base + V * f + q;
+                if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
+                if (a.verify & V_FINGERPRINT) {
+                  const uint64_t g2 = a.global_begin + (uint64_t)it;
+                  fpo += fp_mix(g2); fpw += fp_mix2(g2, (uint64_t)leaf); fpn += 1;
+                }
+              }
+            }
+          }
+        } else if constexpr (sizeof(In) == 4 && MIS) {
           // two aligned LDS.128 per vector (conflict-free) and a uniform
           // shift: the same four elements, the same arithmetic as below
           using V = typename std::conditional<std::is_floating_point<In>::value, float4, int4>::type;
@@ -202,8 +232,8 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
         // ragged last tile: bulk part from smem, the < 16 B tail from global
         const int64_t in_smem = MIS ? len : (len * (int64_t)sizeof(In)) / 16 * 16 / (int64_t)sizeof(In);
         for (int f = warp * 32 + lane; f < vec_per_tile; f += W * 32) {
-          for (int q = 0; q < 4; ++q) {
-            const int64_t off = 4 * (int64_t)f + q;
+          for (int q = 0; q < V; ++q) {
+            const int64_t off = V * (int64_t)f + q;
             if (off >= len) break;
             const In e = (off < in_smem) ? st[off] : x[base + off];
             acc = OpT<OP, Acc>::combine(acc, ElemT<OP, Acc, In>::make(e));
@@ -235,9 +265,9 @@ __global__ void __launch_bounds__(1024, 1) flat_tma_kernel(const __grid_constant
 
 int g_flat_tile = 4096;
 
-template <typename In, typename Acc, int OP, bool VERIFY, bool MIS>
+template <typename In, typename Acc, int OP, bool VERIFY, bool MIS, int V>
 cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
-  auto kern = flat_tma_kernel<In, Acc, OP, VERIFY, MIS>;
+  auto kern = flat_tma_kernel<In, Acc, OP, VERIFY, MIS, V>;
   const size_t smem = (size_t)kStages * stage_stride((uint32_t)(tile * sizeof(In)), MIS);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -258,9 +288,17 @@ cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
 
 template <typename In, typename Acc, int OP>
 cudaError_t launch_v(const NestArgs& a, int W, int tile, cudaStream_t s) {
-  if (((uintptr_t)a.in & 15) != 0)
-    return a.verify ? launch_t<In, Acc, OP, true, true>(a, W, tile, s) : launch_t<In, Acc, OP, false, true>(a, W, tile, s);
-  return a.verify ? launch_t<In, Acc, OP, true, false>(a, W, tile, s) : launch_t<In, Acc, OP, false, false>(a, W, tile, s);
+  const int v = (int)device_levels(a).l[3]->chunk;  // the lane chunk: 1, 2 or 4
+  const bool mis = ((uintptr_t)a.in & 15) != 0;
+  auto go = [&](auto v_c) -> cudaError_t {
+    constexpr int VV = decltype(v_c)::value;
+    if (mis)
+      return a.verify ? launch_t<In, Acc, OP, true, true, VV>(a, W, tile, s) : launch_t<In, Acc, OP, false, true, VV>(a, W, tile, s);
+    return a.verify ? launch_t<In, Acc, OP, true, false, VV>(a, W, tile, s) : launch_t<In, Acc, OP, false, false, VV>(a, W, tile, s);
+  };
+  if (v == 1) return go(std::integral_constant<int, 1>());
+  if (v == 2) return go(std::integral_constant<int, 2>());
+  return go(std::integral_constant<int, 4>());
 }
 
 }  // namespace
@@ -286,10 +324,11 @@ bool flat_matches(const NestArgs& a, const char** why) {
   }
   const int64_t W = a.radix[S_WARP];
   const int64_t tile = k->chunk;
-  if (l->sched != SCHED_STATIC_CHUNK || l->chunk != 4) { *why = "lane must be static(4)"; return false; }
-  if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 128) { *why = "warp must be static(128)"; return false; }
-  if (k->sched != SCHED_STATIC_CHUNK || tile % (128 * W) != 0 || tile * esz > 32768) {
-    *why = "CTA must be static(tile), tile a multiple of 128*W, <= 32 KiB";
+  const int64_t V = l->chunk;
+  if (l->sched != SCHED_STATIC_CHUNK || (V != 1 && V != 2 && V != 4)) { *why = "lane must be static(1|2|4)"; return false; }
+  if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 32 * V) { *why = "warp must be static(32*lane chunk)"; return false; }
+  if (k->sched != SCHED_STATIC_CHUNK || tile % (32 * V * W) != 0 || tile * esz > 32768) {
+    *why = "CTA must be static(tile), tile a multiple of 32*V*W, <= 32 KiB";
     return false;
   }
   if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster must be static(K*tile)"; return false; }

@@ -79,3 +79,9 @@ lv = nests.c5_nest(2)
 lv[-1].chunk = 2  # lane static(2): not the fused flat shape -> the generic interpreter
 nest = H.Nest(lv, device=0, cluster_dim=2, warps_per_cta=4, clusters=148)
 line("flat i64 affine 2^28, lane static(2)", nest, H.make_desc(x, out, n0=n, op=H.OP_AFFINE), n * 8)
+# lane static(1) / static(2) flat nests (warp static(32 V)) on the fused flat kernel
+xf = torch.rand(n, device="cuda")
+for V in (1, 2):
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    nest = H.Nest(nests.flat_nest(2, 4096, V), device=0, cluster_dim=2, warps_per_cta=4, clusters=148)
+    line(f"flat f32 sum 2^28, lane static({V})", nest, H.make_desc(xf, out, n0=n), n * 4)

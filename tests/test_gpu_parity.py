@@ -456,6 +456,33 @@ def test_rowwise_affine_op(H, torch_mod, oracle):
         compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, op=H.OP_AFFINE, C=C, K=K, W=W)
 
 
+@pytest.mark.parametrize("V", [1, 2])
+def test_flat_lane_chunks(H, torch_mod, oracle, V):
+    """The flat nest with lane static(1) / static(2) (warp static(32 V)) on
+    the fused flat kernel: fp32 sums (pairwise inside a lane chunk), int32,
+    fp64 MIN and the int64 AFFINE op; results, owner maps and partials vs
+    the oracle, aligned and off a granule."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    C, K, W = 5, 2, 8
+    rng = np.random.default_rng(70 + V)
+    levels = nests.flat_nest(K=K, tile=4096, vec=V)
+    for n in (0, 5, 4096 * 2 * 5 + 77, 200003):
+        for dt, op in (("f32", H.OP_SUM), ("i32", H.OP_SUM), ("f64", H.OP_MIN), ("i64", H.OP_AFFINE)):
+            if dt == "f32":
+                x = gen.gen_f32(gen.SEED_C5, 0, n)
+            elif dt == "i32":
+                x = gen.gen_i32(gen.SEED_C1, 0, n)
+            elif dt == "f64":
+                x = rng.standard_normal(n)
+            else:
+                x = rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)
+            for mis in ((0, x.itemsize) if n else (0,)):
+                res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis)
+                assert res["kernel"] == "flat_tma"
+                compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
+
+
 def test_rowwise_fused_kernel_small(H, torch_mod, oracle):
     """The fused row-wise kernel (config-2 nest) on 50 x 4096 and ragged
     columns: rows, owner map, per-row lane/warp/CTA partials vs oracle."""
@@ -1004,12 +1031,13 @@ def test_segrows_fuzz(H, torch_mod, oracle, seed):
         assert (count.cpu().numpy()[:nnz] == 1).all()
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(16))
 def test_flat_fuzz(H, torch_mod, oracle, seed):
     """Random flat shapes on the fused flat kernel: length (empty, ragged,
-    several tiles), tile, K, W, C, op, dtype (fp32 / int32 / fp64 / int64,
-    AFFINE over int64) and pointer offset at random; total, owner map and
-    every level's partials vs the oracle."""
+    several tiles), tile, lane chunk (static(1) / static(2) / static(4)), K,
+    W, C, op, dtype (fp32 / int32 / fp64 / int64, AFFINE over int64) and
+    pointer offset at random; total, owner map and every level's partials
+    vs the oracle."""
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     rng = np.random.default_rng(4000 + seed)
@@ -1018,8 +1046,9 @@ def test_flat_fuzz(H, torch_mod, oracle, seed):
               ("f64", H.OP_MIN), ("i64", H.OP_SUM), ("i64", H.OP_AFFINE)]
     dt, op = combos[int(rng.integers(len(combos)))]
     esz = 8 if dt in ("f64", "i64") else 4
-    tile = 128 * W * int(rng.choice([1, 2, 4, 8]))
-    tile = min(tile, 32768 // esz) // (128 * W) * (128 * W) or 128 * W
+    V = int(rng.choice([1, 2, 4]))  # lane static(V), warp static(32 V)
+    tile = 32 * V * W * int(rng.choice([1, 2, 4, 8]))
+    tile = min(tile, 32768 // esz) // (32 * V * W) * (32 * V * W) or 32 * V * W
     C = int(rng.integers(1, 10))
     n = int(rng.choice([0, int(rng.integers(1, 3000)), int(rng.integers(3000, 400000))]))
     if dt == "f32":
@@ -1031,9 +1060,9 @@ def test_flat_fuzz(H, torch_mod, oracle, seed):
     else:
         x = rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)
     mis = int(rng.integers(0, 16 // esz)) * esz if n else 0
-    levels = nests.flat_nest(K=K, tile=tile, vec=4)
+    levels = nests.flat_nest(K=K, tile=tile, vec=V)
     res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis)
-    assert res["kernel"] == "flat_tma", (n, tile, K, W, dt)
+    assert res["kernel"] == "flat_tma", (n, tile, K, W, V, dt)
     compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
 
 
