@@ -148,7 +148,7 @@ __device__ __forceinline__ void store_row(const NestArgs& a, int64_t row, X v) {
   }
 }
 
-template <typename In, int OP, bool VERIFY, int NV>
+template <typename In, int OP, bool VERIFY, int NV, int V = 4>
 __global__ void __launch_bounds__(1024, 1)
     rowwise_kernel(const __grid_constant__ NestArgs a, int W, int qcols, int kStages, int stage_bytes) {
   using P = RwP<In, OP>;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(1024, 1)
     }
   } else {
     // ------------------------------ W consumer warps --------------------
-    const int nvec = NV < 0 ? (lenk + 3) / 4 : qcols / 4;
+    const int nvec = NV < 0 ? (lenk + V - 1) / V : qcols / V;  // lane chunks of V columns
     const uint32_t leader_slot_base = mapa(smem_addr(&slot[0][0]), 0);
     const uint32_t leader_full_base = mapa(smem_addr(&row_full[0]), 0);
     const int push_idx = (int)crank * W + warp;
@@ -252,7 +252,28 @@ __global__ void __launch_bounds__(1024, 1)
       mbar_wait(&full[s], ph);
       const unsigned char* stage = dsm + (size_t)s * seg_bytes;
       P acc = OpT<OP, P>::identity();
-      if constexpr (NV > 0 && F32SUM) {
+      if constexpr (V != 4) {
+        // lane static(1) / static(2): scalar shared loads of the chunk from
+        // the row segment's first element (ragged: `mis` bytes into the
+        // copied granules); a partial last chunk gets identities
+        const uint32_t mis = NV < 0 ? (uint32_t)(((uintptr_t)(x + (row0 + j) * a.ld + col0)) & 15) : 0u;
+        const In* se = (const In*)(stage + mis);
+        for (int f = warp * 32 + lane; f < nvec; f += W * 32) {
+          P t[V];
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            t[k] = (NV >= 0 || V * f + k < lenk) ? ElemT<OP, P, In>::make(se[V * f + k]) : OpT<OP, P>::identity();
+          if constexpr (OP == OP_SUM) {
+            P ps = t[0];
+#pragma unroll
+            for (int k = 1; k < V; ++k) ps += t[k];
+            acc += ps;
+          } else {
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc = OpT<OP, P>::combine(acc, t[k]);
+          }
+        }
+      } else if constexpr (NV > 0 && F32SUM) {
         const float4* st = (const float4*)stage;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
@@ -283,8 +304,8 @@ __global__ void __launch_bounds__(1024, 1)
       }
       if constexpr (VERIFY) {
         for (int f = warp * 32 + lane; f < nvec; f += W * 32)
-          for (int e = 0; e < 4 && 4 * f + e < lenk; ++e) {
-            const int64_t it = (row0 + j) * a.n1 + col0 + 4 * f + e;
+          for (int e = 0; e < V && V * f + e < lenk; ++e) {
+            const int64_t it = (row0 + j) * a.n1 + col0 + V * f + e;
             if (a.verify & V_COVERAGE) { a.owner[it] = leaf; atomicAdd(&a.count[it], 1u); }
           }
       }
@@ -315,9 +336,9 @@ __global__ void __launch_bounds__(1024, 1)
   cluster_sync_all();
 }
 
-template <typename In, int OP, bool V, int NV>
+template <typename In, int OP, bool V, int NV, int LV = 4>
 cudaError_t launch_t(const NestArgs& a, int W, int qcols, int stages, int stage_bytes, cudaStream_t s) {
-  auto kern = rowwise_kernel<In, OP, V, NV>;
+  auto kern = rowwise_kernel<In, OP, V, NV, LV>;
   const size_t smem = (size_t)stages * stage_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -338,6 +359,13 @@ cudaError_t launch_t(const NestArgs& a, int W, int qcols, int stages, int stage_
 
 template <typename In, int OP, bool V>
 cudaError_t launch_nv(const NestArgs& a, int W, int qcols, int stages, int stage_bytes, cudaStream_t s) {
+  const int lv = (int)device_levels(a).l[3]->chunk;  // the lane chunk: 1, 2 or 4
+  if (lv == 1)
+    return rowwise_ragged(a) ? launch_t<In, OP, V, -1, 1>(a, W, qcols, stages, stage_bytes, s)
+                             : launch_t<In, OP, V, 0, 1>(a, W, qcols, stages, stage_bytes, s);
+  if (lv == 2)
+    return rowwise_ragged(a) ? launch_t<In, OP, V, -1, 2>(a, W, qcols, stages, stage_bytes, s)
+                             : launch_t<In, OP, V, 0, 2>(a, W, qcols, stages, stage_bytes, s);
   if (rowwise_ragged(a)) return launch_t<In, OP, V, -1>(a, W, qcols, stages, stage_bytes, s);
   if constexpr (std::is_same<In, float>::value && OP == OP_SUM) {
     const int nv = (qcols % (128 * W) == 0) ? qcols / (128 * W) : 0;
@@ -410,8 +438,14 @@ bool rowwise_matches(const NestArgs& a, const char** why) {
   }
   if (c->loop != 0 || c->sched != SCHED_STATIC) { *why = "rows must be static over clusters"; return false; }
   if (k->loop != 1 || k->sched != SCHED_STATIC) { *why = "columns must be static over CTAs"; return false; }
-  if (w->loop != 1 || w->sched != SCHED_STATIC_CHUNK || w->chunk != 128) { *why = "warp static(128)"; return false; }
-  if (l->loop != 1 || l->sched != SCHED_STATIC_CHUNK || l->chunk != 4) { *why = "lane static(4)"; return false; }
+  if (l->loop != 1 || l->sched != SCHED_STATIC_CHUNK || (l->chunk != 1 && l->chunk != 2 && l->chunk != 4)) {
+    *why = "lane static(1|2|4)";
+    return false;
+  }
+  if (w->loop != 1 || w->sched != SCHED_STATIC_CHUNK || w->chunk != 32 * l->chunk) {
+    *why = "warp static(32 * lane chunk)";
+    return false;
+  }
   const int64_t K = a.K, W = a.radix[S_WARP];
   if (!pow2(K) || !pow2(W) || K * W > kMaxPush || W > 30) { *why = "K, W powers of two, K*W <= 32"; return false; }
   if (((uintptr_t)a.in & (elem_bytes(a) - 1)) || a.ld < a.n1) { *why = "input not element-aligned or ld < n1"; return false; }

@@ -85,3 +85,12 @@ for V in (1, 2):
     out = torch.zeros(1, dtype=torch.float64, device="cuda")
     nest = H.Nest(nests.flat_nest(2, 4096, V), device=0, cluster_dim=2, warps_per_cta=4, clusters=148)
     line(f"flat f32 sum 2^28, lane static({V})", nest, H.make_desc(xf, out, n0=n), n * 4)
+# row sums with lane static(1) / static(2) over the columns (warp static(32 V))
+x = torch.rand(rows * cols, device="cuda")
+for V in (1, 2):
+    lv = nests.c2_nest()
+    lv[-1].chunk, lv[-2].chunk = V, 32 * V
+    out = torch.zeros(rows, dtype=torch.float32, device="cuda")
+    nest = H.Nest(lv, device=0, cluster_dim=2, warps_per_cta=4, clusters=444)
+    line(f"rows f32 sum 65536x4096, lane static({V})", nest,
+         H.make_desc(x, out, n0=rows, n1=cols, ld=cols, nloops=2, keyed=True), rows * cols * 4)

@@ -1090,12 +1090,12 @@ def test_hist_fuzz(H, torch_mod, oracle, seed):
     compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(16))
 def test_rowwise_fuzz(H, torch_mod, oracle, seed):
     """Random dense-row shapes on the fused row-wise kernel: rows, columns,
-    leading dimension, pointer offset, K, W, C, op and dtype at random
-    (ragged or aligned); rows, owner map and every level's partials vs the
-    oracle."""
+    leading dimension, pointer offset, lane chunk (1, 2, 4), K, W, C, op and
+    dtype at random (ragged or aligned); rows, owner map and every level's
+    partials vs the oracle."""
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     rng = np.random.default_rng(3000 + seed)
@@ -1117,8 +1117,10 @@ def test_rowwise_fuzz(H, torch_mod, oracle, seed):
         x = rng.integers(-(1 << 62), 1 << 62, n0 * n1, dtype=np.int64)
     mis = int(rng.integers(0, 16 // x.itemsize)) * x.itemsize
     levels = nests.c2_nest()
+    V = int(rng.choice([1, 2, 4]))  # lane static(V), warp static(32 V) over the columns
+    levels[-1].chunk, levels[-2].chunk = V, 32 * V
     res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=True, op=op, C=C, K=K, W=W, ld=ld, misalign=mis)
-    assert res["kernel"] == "rowwise_tma_dsmem", (n0, n1, ld, K, W, dt, op)
+    assert res["kernel"] == "rowwise_tma_dsmem", (n0, n1, ld, K, W, V, dt, op)
     compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, op=op, C=C, K=K, W=W)
 
 
