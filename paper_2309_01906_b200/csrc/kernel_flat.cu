@@ -27,6 +27,47 @@
 #include "fused_common.cuh"
 
 namespace hpar {
+
+// The flat shape in any of its equivalent spellings: the upper part is
+// cluster static(K*tile) + CTA static(tile), or one collapsed cluster..CTA
+// level static(tile) (the same tile -> CTA map: tile m*(C*K) + c*K + k); the
+// lower part is warp static(32V) + lane static(V), or one collapsed
+// warp..lane level static(V) (the same chunk -> thread map).  Sets tile, V.
+static bool flat_shape(const NestArgs& a, const char** why, int64_t* tile_out, int64_t* v_out) {
+  LevelView v = device_levels(a);
+  int i = 0;
+  int64_t tile = -1, lv = -1;
+  auto sc = [](const DevLevel* L) { return L->sched == SCHED_STATIC_CHUNK; };
+  if (i < v.n && v.l[i]->sfirst == S_CLUSTER && v.l[i]->slast == S_CTA && sc(v.l[i])) {
+    tile = v.l[i]->chunk;
+    i += 1;
+  } else if (i + 1 < v.n && is_level(v.l[i], S_CLUSTER) && is_level(v.l[i + 1], S_CTA) && sc(v.l[i]) &&
+             sc(v.l[i + 1])) {
+    tile = v.l[i + 1]->chunk;
+    if (v.l[i]->chunk != a.K * tile) { *why = "cluster must be static(K*tile)"; return false; }
+    i += 2;
+  } else {
+    *why = "upper levels not cluster static(K*tile) + CTA static(tile) (or cluster..CTA static(tile))";
+    return false;
+  }
+  if (i < v.n && v.l[i]->sfirst == S_WARP && v.l[i]->slast == S_LANE_IN && sc(v.l[i])) {
+    lv = v.l[i]->chunk;
+    i += 1;
+  } else if (i + 1 < v.n && is_level(v.l[i], S_WARP) && is_level(v.l[i + 1], S_LANE) && sc(v.l[i]) &&
+             sc(v.l[i + 1])) {
+    lv = v.l[i + 1]->chunk;
+    if (v.l[i]->chunk != 32 * lv) { *why = "warp must be static(32*lane chunk)"; return false; }
+    i += 2;
+  } else {
+    *why = "lower levels not warp static(32V) + lane static(V) (or warp..lane static(V))";
+    return false;
+  }
+  if (i != v.n) { *why = "extra levels"; return false; }
+  if (lv != 1 && lv != 2 && lv != 4) { *why = "lane chunk must be 1, 2 or 4"; return false; }
+  *tile_out = tile;
+  *v_out = lv;
+  return true;
+}
 namespace {
 
 constexpr int kStages = 4;
@@ -288,7 +329,10 @@ cudaError_t launch_t(const NestArgs& a, int W, int tile, cudaStream_t s) {
 
 template <typename In, typename Acc, int OP>
 cudaError_t launch_v(const NestArgs& a, int W, int tile, cudaStream_t s) {
-  const int v = (int)device_levels(a).l[3]->chunk;  // the lane chunk: 1, 2 or 4
+  int64_t tile_unused, v64 = 4;
+  const char* why;
+  flat_shape(a, &why, &tile_unused, &v64);
+  const int v = (int)v64;  // the lane chunk: 1, 2 or 4
   const bool mis = ((uintptr_t)a.in & 15) != 0;
   auto go = [&](auto v_c) -> cudaError_t {
     constexpr int VV = decltype(v_c)::value;
@@ -315,30 +359,22 @@ bool flat_matches(const NestArgs& a, const char** why) {
   const int64_t esz = (a.in_dtype == DT_F64 || a.in_dtype == DT_I64) ? 8 : 4;
   if (((uintptr_t)a.in & (esz - 1)) != 0) { *why = "input not element-aligned"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
-  LevelView v = device_levels(a);
-  if (v.n != 4) { *why = "needs cluster, CTA, warp, lane levels"; return false; }
-  const DevLevel *c = v.l[0], *k = v.l[1], *w = v.l[2], *l = v.l[3];
-  if (!is_level(c, S_CLUSTER) || !is_level(k, S_CTA) || !is_level(w, S_WARP) || !is_level(l, S_LANE)) {
-    *why = "levels not cluster/CTA/warp/lane";
-    return false;
-  }
+  int64_t tile, V;
+  if (!flat_shape(a, why, &tile, &V)) return false;
   const int64_t W = a.radix[S_WARP];
-  const int64_t tile = k->chunk;
-  const int64_t V = l->chunk;
-  if (l->sched != SCHED_STATIC_CHUNK || (V != 1 && V != 2 && V != 4)) { *why = "lane must be static(1|2|4)"; return false; }
-  if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 32 * V) { *why = "warp must be static(32*lane chunk)"; return false; }
-  if (k->sched != SCHED_STATIC_CHUNK || tile % (32 * V * W) != 0 || tile * esz > 32768) {
-    *why = "CTA must be static(tile), tile a multiple of 32*V*W, <= 32 KiB";
+  if (tile % (32 * V * W) != 0 || tile * esz > 32768) {
+    *why = "tile must be a multiple of 32*V*W, <= 32 KiB";
     return false;
   }
-  if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster must be static(K*tile)"; return false; }
   if (W > 31) { *why = "W > 31 (one producer warp is added)"; return false; }
   return true;
 }
 
 cudaError_t launch_flat(const NestArgs& a, int W, cudaStream_t s, const char** name) {
-  const LevelView v = device_levels(a);
-  const int tile = (int)v.l[1]->chunk;
+  int64_t tile64 = 0, v64 = 0;
+  const char* why;
+  if (!flat_shape(a, &why, &tile64, &v64)) return cudaErrorInvalidValue;
+  const int tile = (int)tile64;
   *name = "flat_tma";
   if (a.in_dtype == DT_F32) {
     if (a.op == OP_SUM) return launch_v<float, double, OP_SUM>(a, W, tile, s);

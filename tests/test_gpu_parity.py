@@ -1031,13 +1031,14 @@ def test_segrows_fuzz(H, torch_mod, oracle, seed):
         assert (count.cpu().numpy()[:nnz] == 1).all()
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(24))
 def test_flat_fuzz(H, torch_mod, oracle, seed):
     """Random flat shapes on the fused flat kernel: length (empty, ragged,
-    several tiles), tile, lane chunk (static(1) / static(2) / static(4)), K,
-    W, C, op, dtype (fp32 / int32 / fp64 / int64, AFFINE over int64) and
-    pointer offset at random; total, owner map and every level's partials
-    vs the oracle."""
+    several tiles), tile, lane chunk (static(1) / static(2) / static(4)), the
+    nest's spelling (separate or collapsed cluster..CTA and warp..lane
+    levels), K, W, C, op, dtype (fp32 / int32 / fp64 / int64, AFFINE over
+    int64) and pointer offset at random; total, owner map and every level's
+    partials vs the oracle."""
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     rng = np.random.default_rng(4000 + seed)
@@ -1060,9 +1061,22 @@ def test_flat_fuzz(H, torch_mod, oracle, seed):
     else:
         x = rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)
     mis = int(rng.integers(0, 16 // esz)) * esz if n else 0
-    levels = nests.flat_nest(K=K, tile=tile, vec=V)
+    # any of the four equivalent spellings: cluster + CTA or cluster..CTA,
+    # warp + lane or warp..lane (the same owner map, so the same kernel)
+    spell = int(rng.integers(4))
+    levels = [H.Level(H.HPAR_GPU, H.HPAR_GPU, H.STATIC)]
+    if spell & 1:
+        levels.append(H.Level(H.HPAR_CLUSTER, H.HPAR_CTA, H.STATIC_CHUNK, chunk=tile))
+    else:
+        levels += [H.Level(H.HPAR_CLUSTER, H.HPAR_CLUSTER, H.STATIC_CHUNK, chunk=K * tile),
+                   H.Level(H.HPAR_CTA, H.HPAR_CTA, H.STATIC_CHUNK, chunk=tile)]
+    if spell & 2:
+        levels.append(H.Level(H.HPAR_WARP, H.HPAR_LANE, H.STATIC_CHUNK, chunk=V))
+    else:
+        levels += [H.Level(H.HPAR_WARP, H.HPAR_WARP, H.STATIC_CHUNK, chunk=32 * V),
+                   H.Level(H.HPAR_LANE, H.HPAR_LANE, H.STATIC_CHUNK, chunk=V)]
     res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis)
-    assert res["kernel"] == "flat_tma", (n, tile, K, W, V, dt)
+    assert res["kernel"] == "flat_tma", (n, tile, K, W, V, dt, spell)
     compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
 
 
