@@ -33,6 +33,47 @@ inline bool is_level(const DevLevel* L, int hw_slot) {
   return L->sfirst == hw_slot && L->slast == hw_slot;
 }
 
+// The flat shape in any of its equivalent spellings: the upper part is
+// cluster static(K*tile) + CTA static(tile), or one collapsed cluster..CTA
+// level static(tile) (the same tile -> CTA map: tile m*(C*K) + c*K + k); the
+// lower part is warp static(32V) + lane static(V), or one collapsed
+// warp..lane level static(V) (the same chunk -> thread map).  Sets tile, V
+// (the flat and histogram kernels check V).
+inline bool flat_nest_shape(const NestArgs& a, const char** why, int64_t* tile_out, int64_t* v_out) {
+  LevelView v = device_levels(a);
+  int i = 0;
+  int64_t tile = -1, lv = -1;
+  auto sc = [](const DevLevel* L) { return L->sched == SCHED_STATIC_CHUNK; };
+  if (i < v.n && v.l[i]->sfirst == S_CLUSTER && v.l[i]->slast == S_CTA && sc(v.l[i])) {
+    tile = v.l[i]->chunk;
+    i += 1;
+  } else if (i + 1 < v.n && is_level(v.l[i], S_CLUSTER) && is_level(v.l[i + 1], S_CTA) && sc(v.l[i]) &&
+             sc(v.l[i + 1])) {
+    tile = v.l[i + 1]->chunk;
+    if (v.l[i]->chunk != a.K * tile) { *why = "cluster must be static(K*tile)"; return false; }
+    i += 2;
+  } else {
+    *why = "upper levels not cluster static(K*tile) + CTA static(tile) (or cluster..CTA static(tile))";
+    return false;
+  }
+  if (i < v.n && v.l[i]->sfirst == S_WARP && v.l[i]->slast == S_LANE_IN && sc(v.l[i])) {
+    lv = v.l[i]->chunk;
+    i += 1;
+  } else if (i + 1 < v.n && is_level(v.l[i], S_WARP) && is_level(v.l[i + 1], S_LANE) && sc(v.l[i]) &&
+             sc(v.l[i + 1])) {
+    lv = v.l[i + 1]->chunk;
+    if (v.l[i]->chunk != 32 * lv) { *why = "warp must be static(32*lane chunk)"; return false; }
+    i += 2;
+  } else {
+    *why = "lower levels not warp static(32V) + lane static(V) (or warp..lane static(V))";
+    return false;
+  }
+  if (i != v.n) { *why = "extra levels"; return false; }
+  *tile_out = tile;
+  *v_out = lv;
+  return true;
+}
+
 // Write the partial of the task at `slot` to every nest level whose last
 // slot is `slot` (verify mode).  `index` = task id below the GPU.
 // elements m4 .. m4+3 of the 8-element concatenation (a, b), m4 in 1..3

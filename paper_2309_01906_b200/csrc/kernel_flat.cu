@@ -28,46 +28,6 @@
 
 namespace hpar {
 
-// The flat shape in any of its equivalent spellings: the upper part is
-// cluster static(K*tile) + CTA static(tile), or one collapsed cluster..CTA
-// level static(tile) (the same tile -> CTA map: tile m*(C*K) + c*K + k); the
-// lower part is warp static(32V) + lane static(V), or one collapsed
-// warp..lane level static(V) (the same chunk -> thread map).  Sets tile, V.
-static bool flat_shape(const NestArgs& a, const char** why, int64_t* tile_out, int64_t* v_out) {
-  LevelView v = device_levels(a);
-  int i = 0;
-  int64_t tile = -1, lv = -1;
-  auto sc = [](const DevLevel* L) { return L->sched == SCHED_STATIC_CHUNK; };
-  if (i < v.n && v.l[i]->sfirst == S_CLUSTER && v.l[i]->slast == S_CTA && sc(v.l[i])) {
-    tile = v.l[i]->chunk;
-    i += 1;
-  } else if (i + 1 < v.n && is_level(v.l[i], S_CLUSTER) && is_level(v.l[i + 1], S_CTA) && sc(v.l[i]) &&
-             sc(v.l[i + 1])) {
-    tile = v.l[i + 1]->chunk;
-    if (v.l[i]->chunk != a.K * tile) { *why = "cluster must be static(K*tile)"; return false; }
-    i += 2;
-  } else {
-    *why = "upper levels not cluster static(K*tile) + CTA static(tile) (or cluster..CTA static(tile))";
-    return false;
-  }
-  if (i < v.n && v.l[i]->sfirst == S_WARP && v.l[i]->slast == S_LANE_IN && sc(v.l[i])) {
-    lv = v.l[i]->chunk;
-    i += 1;
-  } else if (i + 1 < v.n && is_level(v.l[i], S_WARP) && is_level(v.l[i + 1], S_LANE) && sc(v.l[i]) &&
-             sc(v.l[i + 1])) {
-    lv = v.l[i + 1]->chunk;
-    if (v.l[i]->chunk != 32 * lv) { *why = "warp must be static(32*lane chunk)"; return false; }
-    i += 2;
-  } else {
-    *why = "lower levels not warp static(32V) + lane static(V) (or warp..lane static(V))";
-    return false;
-  }
-  if (i != v.n) { *why = "extra levels"; return false; }
-  if (lv != 1 && lv != 2 && lv != 4) { *why = "lane chunk must be 1, 2 or 4"; return false; }
-  *tile_out = tile;
-  *v_out = lv;
-  return true;
-}
 namespace {
 
 constexpr int kStages = 4;
@@ -331,7 +291,7 @@ template <typename In, typename Acc, int OP>
 cudaError_t launch_v(const NestArgs& a, int W, int tile, cudaStream_t s) {
   int64_t tile_unused, v64 = 4;
   const char* why;
-  flat_shape(a, &why, &tile_unused, &v64);
+  flat_nest_shape(a, &why, &tile_unused, &v64);
   const int v = (int)v64;  // the lane chunk: 1, 2 or 4
   const bool mis = ((uintptr_t)a.in & 15) != 0;
   auto go = [&](auto v_c) -> cudaError_t {
@@ -360,7 +320,8 @@ bool flat_matches(const NestArgs& a, const char** why) {
   if (((uintptr_t)a.in & (esz - 1)) != 0) { *why = "input not element-aligned"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
   int64_t tile, V;
-  if (!flat_shape(a, why, &tile, &V)) return false;
+  if (!flat_nest_shape(a, why, &tile, &V)) return false;
+  if (V != 1 && V != 2 && V != 4) { *why = "lane chunk must be 1, 2 or 4"; return false; }
   const int64_t W = a.radix[S_WARP];
   if (tile % (32 * V * W) != 0 || tile * esz > 32768) {
     *why = "tile must be a multiple of 32*V*W, <= 32 KiB";
@@ -373,7 +334,7 @@ bool flat_matches(const NestArgs& a, const char** why) {
 cudaError_t launch_flat(const NestArgs& a, int W, cudaStream_t s, const char** name) {
   int64_t tile64 = 0, v64 = 0;
   const char* why;
-  if (!flat_shape(a, &why, &tile64, &v64)) return cudaErrorInvalidValue;
+  if (!flat_nest_shape(a, &why, &tile64, &v64)) return cudaErrorInvalidValue;
   const int tile = (int)tile64;
   *name = "flat_tma";
   if (a.in_dtype == DT_F32) {

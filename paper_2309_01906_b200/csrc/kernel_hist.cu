@@ -417,18 +417,13 @@ static int hist_regions(const NestArgs& a, int W) {
 bool hist_matches(const NestArgs& a, const char** why) {
   if (a.nloops != 1 || a.keyed || a.op != OP_HIST || a.in_dtype != DT_U8) { *why = "flat u8 hist"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
-  LevelView v = device_levels(a);
-  if (v.n != 4) { *why = "needs cluster, CTA, warp, lane levels"; return false; }
-  const DevLevel *c = v.l[0], *k = v.l[1], *w = v.l[2], *l = v.l[3];
-  if (!is_level(c, S_CLUSTER) || !is_level(k, S_CTA) || !is_level(w, S_WARP) || !is_level(l, S_LANE)) {
-    *why = "levels not cluster/CTA/warp/lane";
-    return false;
-  }
-  const int64_t W = a.radix[S_WARP], tile = k->chunk;
-  if (l->sched != SCHED_STATIC_CHUNK || l->chunk != 16) { *why = "lane static(16)"; return false; }
-  if (w->sched != SCHED_STATIC_CHUNK || w->chunk != 512) { *why = "warp static(512)"; return false; }
-  if (k->sched != SCHED_STATIC_CHUNK || tile % (512 * W) != 0 || tile > 32768) { *why = "CTA static(tile)"; return false; }
-  if (c->sched != SCHED_STATIC_CHUNK || c->chunk != a.K * tile) { *why = "cluster static(K*tile)"; return false; }
+  // the flat shape in any spelling (separate or collapsed cluster..CTA and
+  // warp..lane levels), lane chunks of 16 bytes
+  int64_t tile, V;
+  if (!flat_nest_shape(a, why, &tile, &V)) return false;
+  const int64_t W = a.radix[S_WARP];
+  if (V != 16) { *why = "lane static(16) (warp static(512))"; return false; }
+  if (tile % (512 * W) != 0 || tile > 32768) { *why = "CTA static(tile), a multiple of 512*W, <= 32 KiB"; return false; }
   const int R = hist_regions(a, (int)W);
   if (W > kMaxW || ring_stages(R, (int)tile + 16) < 2) {
     *why = "W <= 16 consumer warps";
@@ -439,7 +434,10 @@ bool hist_matches(const NestArgs& a, const char** why) {
 
 cudaError_t launch_hist(const NestArgs& a, int W, cudaStream_t s, const char** name) {
   *name = "hist256_lanepriv_tma";
-  const int tile = (int)device_levels(a).l[1]->chunk;
+  int64_t tile64 = 0, v64 = 0;
+  const char* why;
+  if (!flat_nest_shape(a, &why, &tile64, &v64)) return cudaErrorInvalidValue;
+  const int tile = (int)tile64;
   const int vpl = (tile % (512 * W) == 0) ? tile / (512 * W) : 0;
   const int R = hist_regions(a, W);
   if (a.verify) {

@@ -1080,11 +1080,12 @@ def test_flat_fuzz(H, torch_mod, oracle, seed):
     compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(20))
 def test_hist_fuzz(H, torch_mod, oracle, seed):
     """Random shapes on the histogram kernel: length, tile, K, W (private or
-    shared lane-table regions), C, pointer offset, uniform / skewed / constant
-    bytes; bins, owner map and every level's partials vs the oracle."""
+    shared lane-table regions), C, pointer offset, the nest's spelling
+    (separate or collapsed levels), uniform / skewed / constant bytes; bins,
+    owner map and every level's partials vs the oracle."""
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     rng = np.random.default_rng(5000 + seed)
@@ -1097,9 +1098,20 @@ def test_hist_fuzz(H, torch_mod, oracle, seed):
     x = (gen.gen_u8(gen.SEED_C4 + seed, 0, n) if kind == 0 else gen.gen_u8_zipf(gen.SEED_C4 + seed, 0, n)
          if kind == 1 else np.full(n, int(rng.integers(256)), dtype=np.uint8))
     mis = int(rng.integers(0, 16)) if n else 0
-    levels = nests.c4_nest(K=K, tile=tile)
+    spell = int(rng.integers(4))  # separate or collapsed cluster..CTA / warp..lane levels
+    levels = [H.Level(H.HPAR_GPU, H.HPAR_GPU, H.STATIC)]
+    if spell & 1:
+        levels.append(H.Level(H.HPAR_CLUSTER, H.HPAR_CTA, H.STATIC_CHUNK, chunk=tile))
+    else:
+        levels += [H.Level(H.HPAR_CLUSTER, H.HPAR_CLUSTER, H.STATIC_CHUNK, chunk=K * tile),
+                   H.Level(H.HPAR_CTA, H.HPAR_CTA, H.STATIC_CHUNK, chunk=tile)]
+    if spell & 2:
+        levels.append(H.Level(H.HPAR_WARP, H.HPAR_LANE, H.STATIC_CHUNK, chunk=16))
+    else:
+        levels += [H.Level(H.HPAR_WARP, H.HPAR_WARP, H.STATIC_CHUNK, chunk=512),
+                   H.Level(H.HPAR_LANE, H.HPAR_LANE, H.STATIC_CHUNK, chunk=16)]
     res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, misalign=mis)
-    assert res["kernel"].startswith("hist256_lanepriv"), (n, tile, K, W)
+    assert res["kernel"].startswith("hist256_lanepriv"), (n, tile, K, W, spell)
     assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
     compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
 
