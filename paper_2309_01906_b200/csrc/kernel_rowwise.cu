@@ -53,6 +53,25 @@ constexpr int kMaxPush = 32;    // K*W <= 32 warp partials per row
 // granules and the lanes shift by the row's offset (load_quad).
 bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
+// the lane chunk V of the columns' warp / lane part — warp static(32V) +
+// lane static(V), or one collapsed warp..lane level static(V) (the same
+// chunk -> thread map) — or -1
+int rowwise_lane_chunk(const NestArgs& a) {
+  LevelView v = device_levels(a);
+  int64_t V = -1;
+  if (v.n == 4) {
+    const DevLevel *w = v.l[2], *l = v.l[3];
+    if (!is_level(w, S_WARP) || !is_level(l, S_LANE) || w->loop != 1 || l->loop != 1) return -1;
+    if (w->sched != SCHED_STATIC_CHUNK || l->sched != SCHED_STATIC_CHUNK || w->chunk != 32 * l->chunk) return -1;
+    V = l->chunk;
+  } else if (v.n == 3) {
+    const DevLevel* t = v.l[2];
+    if (t->sfirst != S_WARP || t->slast != S_LANE_IN || t->loop != 1 || t->sched != SCHED_STATIC_CHUNK) return -1;
+    V = t->chunk;
+  }
+  return (V == 1 || V == 2 || V == 4) ? (int)V : -1;
+}
+
 int elem_bytes(const NestArgs& a) { return (a.in_dtype == DT_F64 || a.in_dtype == DT_I64) ? 8 : 4; }
 
 // rows the aligned path cannot copy whole: n1 not a multiple of 4K, or rows
@@ -214,12 +233,14 @@ __global__ void __launch_bounds__(1024, 1)
   } else if (warp == W + 1) {
     // ------------------------------ combiner warp (leader CTA only) ----
     if (crank == 0) {
-      const int rpp = 32 / npush;          // rows per pass
+      // rows per pass: at most the slot ring's depth (K*W = 1 would give 32
+      // lanes 32 rows on 16 slots: two rows per slot in one pass)
+      const int rpp = 32 / npush < kSlots ? 32 / npush : kSlots;
       const int g = lane / npush;          // this lane's row within the pass
       const int e = lane % npush;          // warp partial index within the row
       for (uint32_t j0 = 0; j0 < nrows; j0 += rpp) {
         const uint32_t j = j0 + g;
-        const bool live = j < nrows;
+        const bool live = g < rpp && j < nrows;
         const int s = (int)(j % kSlots);
         X v = OpT<OP, X>::identity();
         if (live) {
@@ -359,7 +380,7 @@ cudaError_t launch_t(const NestArgs& a, int W, int qcols, int stages, int stage_
 
 template <typename In, int OP, bool V>
 cudaError_t launch_nv(const NestArgs& a, int W, int qcols, int stages, int stage_bytes, cudaStream_t s) {
-  const int lv = (int)device_levels(a).l[3]->chunk;  // the lane chunk: 1, 2 or 4
+  const int lv = rowwise_lane_chunk(a);  // the lane chunk: 1, 2 or 4
   if (lv == 1)
     return rowwise_ragged(a) ? launch_t<In, OP, V, -1, 1>(a, W, qcols, stages, stage_bytes, s)
                              : launch_t<In, OP, V, 0, 1>(a, W, qcols, stages, stage_bytes, s);
@@ -430,20 +451,13 @@ bool rowwise_matches(const NestArgs& a, const char** why) {
   if (a.verify & V_FINGERPRINT) { *why = "fingerprints not produced by the rowwise kernel"; return false; }
   if (a.lane_w != 1) { *why = "lane partition"; return false; }
   LevelView v = device_levels(a);
-  if (v.n != 4) { *why = "needs cluster, CTA, warp, lane levels"; return false; }
-  const DevLevel *c = v.l[0], *k = v.l[1], *w = v.l[2], *l = v.l[3];
-  if (!is_level(c, S_CLUSTER) || !is_level(k, S_CTA) || !is_level(w, S_WARP) || !is_level(l, S_LANE)) {
-    *why = "levels not cluster/CTA/warp/lane";
-    return false;
-  }
+  if (v.n != 4 && v.n != 3) { *why = "needs cluster, CTA, warp + lane (or warp..lane) levels"; return false; }
+  const DevLevel *c = v.l[0], *k = v.l[1];
+  if (!is_level(c, S_CLUSTER) || !is_level(k, S_CTA)) { *why = "levels not cluster / CTA"; return false; }
   if (c->loop != 0 || c->sched != SCHED_STATIC) { *why = "rows must be static over clusters"; return false; }
   if (k->loop != 1 || k->sched != SCHED_STATIC) { *why = "columns must be static over CTAs"; return false; }
-  if (l->loop != 1 || l->sched != SCHED_STATIC_CHUNK || (l->chunk != 1 && l->chunk != 2 && l->chunk != 4)) {
-    *why = "lane static(1|2|4)";
-    return false;
-  }
-  if (w->loop != 1 || w->sched != SCHED_STATIC_CHUNK || w->chunk != 32 * l->chunk) {
-    *why = "warp static(32 * lane chunk)";
+  if (rowwise_lane_chunk(a) < 0) {
+    *why = "columns over warps / lanes: warp static(32V) + lane static(V), or warp..lane static(V), V = 1|2|4";
     return false;
   }
   const int64_t K = a.K, W = a.radix[S_WARP];

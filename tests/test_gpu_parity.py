@@ -1116,7 +1116,7 @@ def test_hist_fuzz(H, torch_mod, oracle, seed):
     compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(24))
 def test_rowwise_fuzz(H, torch_mod, oracle, seed):
     """Random dense-row shapes on the fused row-wise kernel: rows, columns,
     leading dimension, pointer offset, lane chunk (1, 2, 4), K, W, C, op and
@@ -1145,6 +1145,8 @@ def test_rowwise_fuzz(H, torch_mod, oracle, seed):
     levels = nests.c2_nest()
     V = int(rng.choice([1, 2, 4]))  # lane static(V), warp static(32 V) over the columns
     levels[-1].chunk, levels[-2].chunk = V, 32 * V
+    if rng.random() < 0.5:  # the collapsed spelling: one warp..lane level static(V)
+        levels = levels[:-2] + [H.Level(H.HPAR_WARP, H.HPAR_LANE, H.STATIC_CHUNK, loop=1, chunk=V)]
     res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=True, op=op, C=C, K=K, W=W, ld=ld, misalign=mis)
     assert res["kernel"] == "rowwise_tma_dsmem", (n0, n1, ld, K, W, V, dt, op)
     compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=True, op=op, C=C, K=K, W=W)
