@@ -88,7 +88,10 @@ int64_t rowwise_stage_bytes(const NestArgs& a) {
   const int64_t esz = elem_bytes(a);
   if (!rowwise_ragged(a)) return a.n1 / a.K * esz;
   const int64_t qmax = (a.n1 + a.K - 1) / a.K;
-  return ((qmax * esz + 15) / 16 + 1) * 16;
+  // the lanes read whole 16-byte granules: a 4-element vector spans
+  // esz / 4 granules plus one for the shift, so the last (partial) vector
+  // reaches granule (esz / 4) * ceil(qmax / 4) — allocate through it
+  return ((qmax + 3) / 4 * (esz / 4) + 1) * 16;
 }
 
 // Element and partial types.  In: the input element; P: the lane / warp

@@ -1,6 +1,7 @@
 """GPU parity: libhpar.so (through the C ABI) against the oracle, element by
 element, on seeded inputs.  Bit-exact for integers, coverage maps and bins;
 1e-5 relative for fp32 (north_star).  Runs on the B200 box (-m gpu)."""
+import os
 import random
 
 import numpy as np
@@ -8,6 +9,9 @@ import pytest
 
 from inputs import gen
 from tests.nestutil import assert_rel, fanouts, oracle_levels
+
+# HPAR_FUZZ_N=<n>: run every randomized fuzz test with n seeds (a long sweep)
+FUZZ_N = int(os.environ.get("HPAR_FUZZ_N", "0"))
 
 pytestmark = pytest.mark.gpu
 
@@ -963,7 +967,7 @@ def test_segmented_fuzz(H, torch_mod, oracle, seed):
         assert (count.cpu().numpy()[:nnz] == 1).all()
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(FUZZ_N or 12))
 def test_segrows_fuzz(H, torch_mod, oracle, seed):
     """Random CSR shapes on the CSR rows kernel: empty / short / medium /
     long (> 4096) rows in random order, a random op and dtype (MIN / MAX over
@@ -1031,7 +1035,7 @@ def test_segrows_fuzz(H, torch_mod, oracle, seed):
         assert (count.cpu().numpy()[:nnz] == 1).all()
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(FUZZ_N or 24))
 def test_flat_fuzz(H, torch_mod, oracle, seed):
     """Random flat shapes on the fused flat kernel: length (empty, ragged,
     several tiles), tile, lane chunk (static(1) / static(2) / static(4)), the
@@ -1080,7 +1084,7 @@ def test_flat_fuzz(H, torch_mod, oracle, seed):
     compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
 
 
-@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("seed", range(FUZZ_N or 20))
 def test_hist_fuzz(H, torch_mod, oracle, seed):
     """Random shapes on the histogram kernel: length, tile, K, W (private or
     shared lane-table regions), C, pointer offset, the nest's spelling
@@ -1116,7 +1120,7 @@ def test_hist_fuzz(H, torch_mod, oracle, seed):
     compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(FUZZ_N or 24))
 def test_rowwise_fuzz(H, torch_mod, oracle, seed):
     """Random dense-row shapes on the fused row-wise kernel: rows, columns,
     leading dimension, pointer offset, lane chunk (1, 2, 4), K, W, C, op and
