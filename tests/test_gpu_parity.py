@@ -872,6 +872,40 @@ def test_teams_affine_op(H, torch_mod, oracle):
         compare(oracle, H, levels, res, x, n0=n0, n1=n1, op=H.OP_AFFINE, C=C, K=2, W=4)
 
 
+@pytest.mark.parametrize("seed", range(FUZZ_N or 16))
+def test_teams_fuzz(H, torch_mod, oracle, seed):
+    """Random two-level teams x threads nests (config-1 shape: teams =
+    cluster..CTA static over rows, threads = warp..lane static(c) over
+    columns) on the fused teams kernel: rows, columns, ld, chunk c, K, W, C,
+    op and dtype (AFFINE over int64) at random; total, owner map and every
+    level's partials vs the oracle."""
+    torch = torch_mod
+    rng = np.random.default_rng(6000 + seed)
+    n0 = int(rng.integers(1, 300))
+    n1 = int(rng.choice([int(rng.integers(1, 64)), int(rng.integers(64, 3000))]))
+    ld = n1 + int(rng.choice([0, 0, int(rng.integers(1, 9))]))
+    K, W = int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 8]))
+    C = int(rng.integers(1, 12))
+    chunk = int(rng.choice([1, 2, 3, 4, 8, 16]))
+    combos = [("i32", H.OP_SUM), ("i32", H.OP_MAX), ("f32", H.OP_SUM), ("f64", H.OP_MIN), ("i64", H.OP_SUM),
+              ("i64", H.OP_AFFINE)]
+    dt, op = combos[int(rng.integers(len(combos)))]
+    if dt == "i32":
+        x = gen.gen_i32(gen.SEED_C1 + seed, 0, n0 * n1)
+    elif dt == "f32":
+        x = gen.gen_f32(gen.SEED_C1 + seed, 0, n0 * n1)
+    elif dt == "f64":
+        x = rng.standard_normal(n0 * n1)
+    else:
+        x = rng.integers(-(1 << 62), 1 << 62, n0 * n1, dtype=np.int64)
+    levels = [H.Level(H.HPAR_GPU, H.HPAR_GPU, H.STATIC, loop=0),
+              H.Level(H.HPAR_CLUSTER, H.HPAR_CTA, H.STATIC, loop=0),
+              H.Level(H.HPAR_WARP, H.HPAR_LANE, H.STATIC_CHUNK, loop=1, chunk=chunk)]
+    res = run_nest(H, torch, levels, x, n0=n0, n1=n1, op=op, C=C, K=K, W=W, ld=ld)
+    assert res["kernel"] == "teams_threads", (n0, n1, chunk, K, W, dt)
+    compare(oracle, H, levels, res, x, n0=n0, n1=n1, op=op, C=C, K=K, W=W)
+
+
 def test_generic_keyed_dynamic_repeated_calls(H, torch_mod, oracle):
     """Regression: in keyed mode every CTA of a cluster must be done before the
     cluster's leader arrives at the grid ticket (whose last arriver resets the
@@ -925,7 +959,7 @@ def test_segmented_nnz_balanced_ranks(H, torch_mod, oracle, G):
     assert_rel(got, oracle.segsum_f32(v, off))
 
 
-@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("seed", range(FUZZ_N or 10))
 def test_segmented_fuzz(H, torch_mod, oracle, seed):
     """Random CSR shapes through the fused kernel: empty / short / medium /
     split (> 4096) rows in random order, nnz with any residue mod 4, and
