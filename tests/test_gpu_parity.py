@@ -213,7 +213,7 @@ def test_generic_random_flat_nests(H, torch_mod, oracle):
     torch = torch_mod
     rng = random.Random(2309)
     done = 0
-    while done < 40:
+    while done < (FUZZ_N or 40):
         levels = random_flat_nest(H, rng, 0)
         C, K, W = rng.choice([1, 3, 5]), rng.choice([1, 2, 4]), rng.choice([1, 2, 4])
         n = rng.randint(0, 7000)
@@ -231,6 +231,40 @@ def test_generic_random_flat_nests(H, torch_mod, oracle):
         compare(oracle, H, levels, res, x, n0=n, C=C, K=K, W=W)
         done += 1
         assert Ts
+
+
+def test_generic_random_two_loop_nests(H, torch_mod, oracle):
+    """Random two-loop dense nests on the generic interpreter (the runs of
+    consecutive positions it maps once, chain_map_run): a random cut of the
+    hierarchy between the rows' levels (loop 0) and the columns' levels
+    (loop 1), random collapses and static / static(c) schedules, keyed or
+    total, ragged shapes; results, owner maps and partials vs the oracle."""
+    torch = torch_mod
+    rng = random.Random(2310)
+    hw = [H.HPAR_GPU, H.HPAR_CLUSTER, H.HPAR_CTA, H.HPAR_WARP, H.HPAR_LANE]
+    done = tries = 0
+    while done < (FUZZ_N or 30) and tries < 20 * (FUZZ_N or 30):
+        tries += 1
+        cuts = sorted(rng.sample(range(1, 5), rng.randint(1, 4)))
+        bounds = [0] + cuts + [5]
+        nl = len(bounds) - 1
+        split = rng.randint(1, nl - 1) if nl > 1 else 1  # levels [0, split) on loop 0, the rest on loop 1
+        levels = []
+        for i in range(nl):
+            sch, c = rng.choice([(0, 0), (1, 1), (1, 3), (1, 8)])
+            levels.append(H.Level(hw[bounds[i]], hw[bounds[i + 1] - 1], sch, loop=0 if i < split else 1, chunk=c))
+        keyed = rng.random() < 0.5
+        C, K, W = rng.choice([1, 3, 5]), rng.choice([1, 2, 4]), rng.choice([1, 2, 4])
+        n0, n1 = rng.randint(1, 60), rng.randint(1, 400)
+        x = gen.gen_i32(done + 900, 0, n0 * n1) if done % 2 == 0 else gen.gen_f32(done + 900, 0, n0 * n1)
+        try:
+            res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=keyed, C=C, K=K, W=W)
+        except H.HparError as e:  # nests the model rejects (e.g. a keyed combine needing a missing barrier)
+            assert e.code in (H.HPAR_E_CAPABILITY, H.HPAR_E_INVALID, H.HPAR_E_UNSUPPORTED), e
+            continue
+        compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=keyed, C=C, K=K, W=W)
+        done += 1
+    assert done >= (FUZZ_N or 30) // 2
 
 
 def test_generic_min_max(H, torch_mod, oracle):
@@ -828,7 +862,7 @@ def test_ordered_affine_op(H, torch_mod, oracle):
     torch = torch_mod
     rng = random.Random(86)
     done = 0
-    while done < 25:
+    while done < (FUZZ_N or 25):
         levels = random_flat_nest(H, rng, 0)
         for l in levels:
             if l.schedule == H.NONE:
