@@ -1,5 +1,7 @@
 """NEXT f3 on the GPU: the 5-point stencil kernel (kernel_stencil.cu) and
 the §4 device-level ghost maps, bit-exact against oracle/ghostmap.py."""
+import os
+
 import numpy as np
 import pytest
 
@@ -137,3 +139,29 @@ def test_stencil_division_special_values(env):
     want = G.stencil5(A, 1)
     assert np.array_equal(got.view(np.uint32)[1, 1::2][~np.isnan(vals)], want.view(np.uint32)[1, 1::2][~np.isnan(vals)])
     assert np.array_equal(np.isnan(got), np.isnan(want))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("HPAR_FUZZ_N", "0")) or 16))
+def test_stencil_fuzz(env, seed):
+    """Random single-sibling stencils: array shape, row pitch (a multiple of
+    4 >= the width), a random from-section inside the array and one sweep;
+    the from-section vs the oracle's numpy step, every other cell of `out`
+    untouched (P:383)."""
+    torch, H, nest = env
+    rng = np.random.default_rng(7000 + seed)
+    R, C = int(rng.integers(1, 400)), int(rng.integers(1, 700))
+    ld = (C + 3) // 4 * 4 + 4 * int(rng.integers(0, 4))
+    A = field(R, C, seed=gen.SEED_C5 + seed)
+    r0, c0 = int(rng.integers(0, R)), int(rng.integers(0, C))
+    nr, nc = int(rng.integers(1, R - r0 + 1)), int(rng.integers(1, C - c0 + 1))
+    a = torch.zeros((R, ld), dtype=torch.float32, device="cuda")
+    a[:, :C] = torch.from_numpy(A).cuda()
+    b = torch.full_like(a, -7.0)
+    H.hpar_stencil5(nest, H.stencil_desc(a, b, ld, H.Rect((0, 0), (R, C)), H.Rect((r0, c0), (nr, nc)), (R, C)))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "stencil5_tma"
+    got = b.cpu().numpy()[:, :C]
+    want = np.full_like(A, -7.0)
+    want[r0:r0 + nr, c0:c0 + nc] = G.stencil5(A, 1)[r0:r0 + nr, c0:c0 + nc]
+    assert np.array_equal(got, want), (R, C, ld, r0, c0, nr, nc)
+    assert (b.cpu().numpy()[:, C:] == -7.0).all(), "padding columns written"
