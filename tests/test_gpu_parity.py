@@ -918,7 +918,7 @@ def test_teams_fuzz(H, torch_mod, oracle, seed):
     n0 = int(rng.integers(1, 300))
     n1 = int(rng.choice([int(rng.integers(1, 64)), int(rng.integers(64, 3000))]))
     ld = n1 + int(rng.choice([0, 0, int(rng.integers(1, 9))]))
-    K, W = int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 8]))
+    K, W = int(rng.choice([1, 2, 4, 8])), int(rng.choice([1, 2, 4, 8, 16]))
     C = int(rng.integers(1, 12))
     chunk = int(rng.choice([1, 2, 3, 4, 8, 16]))
     combos = [("i32", H.OP_SUM), ("i32", H.OP_MAX), ("f32", H.OP_SUM), ("f64", H.OP_MIN), ("i64", H.OP_SUM),
@@ -1114,7 +1114,7 @@ def test_flat_fuzz(H, torch_mod, oracle, seed):
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     rng = np.random.default_rng(4000 + seed)
-    K, W = int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 8]))
+    K, W = int(rng.choice([1, 2, 4, 8])), int(rng.choice([1, 2, 4, 8, 16]))
     combos = [("f32", H.OP_SUM), ("f32", H.OP_MAX), ("i32", H.OP_SUM), ("i32", H.OP_MIN), ("f64", H.OP_SUM),
               ("f64", H.OP_MIN), ("i64", H.OP_SUM), ("i64", H.OP_AFFINE)]
     dt, op = combos[int(rng.integers(len(combos)))]
@@ -1161,7 +1161,7 @@ def test_hist_fuzz(H, torch_mod, oracle, seed):
     from paper_2309_01906_b200 import nests
     torch = torch_mod
     rng = np.random.default_rng(5000 + seed)
-    K, W = int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 6, 8]))
+    K, W = int(rng.choice([1, 2, 4, 8])), int(rng.choice([1, 2, 4, 6, 8, 12, 16]))
     tile = 512 * W * int(rng.choice([1, 2, 4]))
     tile = min(tile, 32768) // (512 * W) * (512 * W) or 512 * W
     C = int(rng.integers(1, 8))
@@ -1200,7 +1200,9 @@ def test_rowwise_fuzz(H, torch_mod, oracle, seed):
     n0 = int(rng.integers(1, 120))
     n1 = int(rng.choice([int(rng.integers(1, 40)), int(rng.integers(40, 5000))]))
     ld = n1 + int(rng.choice([0, 0, int(rng.integers(1, 9))]))
-    K, W = int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 8]))
+    K, W = int(rng.choice([1, 2, 4, 8])), int(rng.choice([1, 2, 4, 8]))
+    if K * W > 32:
+        W = 32 // K
     C = int(rng.integers(1, 12))
     combos = [("f32", H.OP_SUM), ("f32", H.OP_MIN), ("f64", H.OP_SUM), ("f64", H.OP_MAX), ("i32", H.OP_SUM),
               ("i64", H.OP_MIN), ("i64", H.OP_AFFINE)]
