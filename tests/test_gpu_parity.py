@@ -1017,6 +1017,11 @@ def test_segmented_fuzz(H, torch_mod, oracle, seed):
         spikes = rng.random(nnz) < 0.001
         v = np.where(spikes, (10.0 ** rng.uniform(-20, 20, nnz)).astype(np.float32), v).astype(np.float32)
     nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=int(rng.integers(1, 9)))
+    if seed % 4 == 3:  # a CSR slice: rows start at b0 > 0, the b0 values before them are NaN (never read into a row)
+        b0 = int(rng.integers(1, 41))
+        off = off + b0
+        v = np.concatenate([np.full(b0, np.nan, dtype=np.float32), v])
+        nnz = int(off[-1])
     xd = torch.from_numpy(v).cuda() if nnz else torch.zeros(4, dtype=torch.float32, device="cuda")
     offd = torch.from_numpy(off).cuda()
     out = torch.full((rows,), -1.0, dtype=torch.float64, device="cuda")
@@ -1032,7 +1037,8 @@ def test_segmented_fuzz(H, torch_mod, oracle, seed):
         assert nest.last_kernel() == "segmented_csr"
         assert_rel(out.cpu().numpy(), want)
     if nnz:
-        assert (count.cpu().numpy()[:nnz] == 1).all()
+        cnt = count.cpu().numpy()[:nnz]
+        assert (cnt[int(off[0]):] == 1).all() and (cnt[:int(off[0])] == 0).all()
 
 
 @pytest.mark.parametrize("seed", range(FUZZ_N or 12))
@@ -1064,6 +1070,12 @@ def test_segrows_fuzz(H, torch_mod, oracle, seed):
         v = rng.integers(-(1 << 31), (1 << 31) - 1, nnz, dtype=np.int64).astype(np.int32)
     else:
         v = rng.integers(-(1 << 62), 1 << 62, nnz, dtype=np.int64)
+    if seed % 4 == 3:  # a CSR slice: rows start at b0 > 0 after b0 poison values no row covers
+        b0 = int(rng.integers(1, 41))
+        off = off + b0
+        poison = np.full(b0, np.nan if v.dtype.kind == "f" else np.iinfo(v.dtype).max // 3, dtype=v.dtype)
+        v = np.concatenate([poison, v])
+        nnz = int(off[-1])
     lpl = int(rng.choice([8, 16]))
     nest = H.Nest(nests.c3_fast_nest(lane_chunk=lpl), device=0, cluster_dim=2, warps_per_cta=8,
                   clusters=int(rng.integers(1, 9)))
@@ -1100,7 +1112,8 @@ def test_segrows_fuzz(H, torch_mod, oracle, seed):
         else:
             assert np.array_equal(got, want)
     if nnz:
-        assert (count.cpu().numpy()[:nnz] == 1).all()
+        cnt = count.cpu().numpy()[:nnz]
+        assert (cnt[int(off[0]):] == 1).all() and (cnt[:int(off[0])] == 0).all()
 
 
 @pytest.mark.parametrize("seed", range(FUZZ_N or 24))
