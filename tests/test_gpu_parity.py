@@ -267,6 +267,39 @@ def test_generic_random_two_loop_nests(H, torch_mod, oracle):
     assert done >= (FUZZ_N or 30) // 2
 
 
+@pytest.mark.parametrize("seed", range(FUZZ_N or 12))
+def test_generic_csr_fuzz(H, torch_mod, oracle, seed):
+    """Random CSR nests of the generic form (config-3 shape: rows
+    dynamic(c) over teams, lanes(w) partitions over the rows, nonzeros
+    static(1) over a row's lane group) on the generic interpreter: random
+    rows_chunk, width, geometry, op and dtype; every row vs the oracle, every
+    nonzero visited once (dynamic schedules: counts, not owner maps)."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    rng = np.random.default_rng(8000 + seed)
+    rows = int(rng.integers(1, 1500))
+    lens = np.where(rng.random(rows) < 0.2, 0, rng.geometric(0.1, rows))
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    nnz = int(off[-1])
+    combos = [("f32", H.OP_SUM), ("f32", H.OP_MAX), ("i32", H.OP_SUM), ("i64", H.OP_MIN), ("f64", H.OP_SUM)]
+    dt, op = combos[int(rng.integers(len(combos)))]
+    if dt == "f32":
+        v = gen.gen_f32(gen.SEED_C3 + seed, 0, nnz)
+    elif dt == "i32":
+        v = gen.gen_i32(gen.SEED_C1 + seed, 0, nnz)
+    elif dt == "i64":
+        v = rng.integers(-(1 << 62), 1 << 62, nnz, dtype=np.int64)
+    else:
+        v = rng.standard_normal(nnz)
+    levels = nests.c3_nest(with_gpu=True, rows_chunk=int(rng.choice([1, 3, 16, 64])),
+                           width=int(rng.choice([1, 2, 4, 8, 16, 32])))
+    C, K, W = int(rng.integers(1, 8)), int(rng.choice([1, 2, 4])), int(rng.choice([1, 2, 4, 8]))
+    res = run_nest(H, torch, levels, v, n0=rows, offsets=off, keyed=True, op=op, C=C, K=K, W=W, partials=False)
+    assert res["kernel"] == "generic"
+    compare(oracle, H, levels, res, v, n0=rows, offsets=off, keyed=True, op=op, C=C, K=K, W=W, dynamic=True,
+            partials=False)
+
+
 def test_generic_min_max(H, torch_mod, oracle):
     torch = torch_mod
     levels = [H.Level(H.HPAR_CLUSTER, H.HPAR_CTA, 1, chunk=5), H.Level(H.HPAR_WARP, H.HPAR_LANE, 0)]
