@@ -264,7 +264,9 @@ typedef struct {
                             a workspace copy), reading never past the granule of a valid
                             element                                                        */
   int64_t n0;            /* GLOBAL extent of loop 0 (sharded over the GPU level)           */
-  int64_t n1;            /* dense extent of loop 1 (0 for CSR)                              */
+  int64_t n1;            /* dense extent of loop 1; CSR: the number of values
+                            (offsets[n0_local]), or 0 = read it from the device (one
+                            host synchronisation per call; not inside graph capture)   */
   int64_t ld;            /* dense row stride in elements (>= n1)                            */
   const int64_t* offsets;/* CSR: device int64 [n0_local + 1], local row offsets, or NULL  */
   int64_t max_inner;     /* CSR: max row length (required with schedule NONE on loop 1, and

@@ -796,6 +796,21 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   A.n1 = d->n1;
   A.ld = d->ld ? d->ld : d->n1;
   A.offsets = d->offsets;
+  // CSR: the fused CSR kernels need the value count (nnz = offsets[n0_local]);
+  // hpar.h lets a caller pass n1 = 0 for CSR, so read it from the device then
+  // (8 bytes and one host synchronisation; inside graph capture that is not
+  // possible: the caller passes n1 = nnz there)
+  if (csr && d->n1 == 0 && local > 0) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(HPAR_E_INVALID, "CSR call inside graph capture with n1 = 0: pass desc->n1 = offsets[n0_local]");
+    int64_t last = 0;
+    CUDA_TRY(cudaMemcpyAsync(&last, d->offsets + local, 8, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (last < 0) return fail(HPAR_E_INVALID, "CSR offsets[n0_local] = %lld < 0", (long long)last);
+    A.n1 = last;
+  }
   A.out = d->out;
   for (int a = 0; a < HPAR_MAX_NEST; ++a) A.partials[a] = d->level_partials[a];
   A.owner = d->coverage_owner;
@@ -892,7 +907,7 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
     // nnz it was built for, never of the current call's: a later call with
     // fewer nonzeros keeps the same offsets, so the self-reset tickets and the
     // all-ones empty queue slots stay where the kernel looks for them.
-    const int64_t nnz = d->n1;
+    const int64_t nnz = A.n1;
     {
       bool span_ok = true, synced = false;
       // (error_flag's 64 device bytes serve as the check's scratch word)
@@ -930,7 +945,7 @@ extern "C" hpar_status hpar_parallel_for_reduce(hpar_nest_t n, const hpar_reduce
   } else if (segrows_matches(A, &why)) {
     // CSR rows for the other ops / dtypes: the same nest, a segmented
     // reduction per window (kernel_segrows.cu); workspace keyed on its nnz
-    const int64_t nnz = d->n1;
+    const int64_t nnz = A.n1;
     if (nnz > n->sr_ws_nnz) {
       const size_t need = segrows_ws_bytes(nnz);
       cudaFree(n->sr_ws);

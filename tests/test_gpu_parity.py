@@ -65,8 +65,9 @@ def test_device_generator_matches_numpy(inputs_lib, torch_mod):
 
 # ---------------------------------------------------------------------------
 def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, C=4, K=2, W=4,
-             partials=True, coverage=True, max_inner=0, out_f64=True, misalign=0, ld=0):
-    nest = H.Nest(levels, device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
+             partials=True, coverage=True, max_inner=0, out_f64=True, misalign=0, ld=0, nest=None):
+    if nest is None:  # (a caller may pass one Nest to reuse across calls)
+        nest = H.Nest(levels, device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
     nloops = 2 if (n1 or offsets is not None) else 1
     if offsets is not None:
         n_iter = int(offsets[-1])
@@ -298,6 +299,101 @@ def test_generic_csr_fuzz(H, torch_mod, oracle, seed):
     assert res["kernel"] == "generic"
     compare(oracle, H, levels, res, v, n0=rows, offsets=off, keyed=True, op=op, C=C, K=K, W=W, dynamic=True,
             partials=False)
+
+
+@pytest.mark.parametrize("family", ["flat", "hist", "rowwise", "teams", "segrows"])
+def test_nest_reuse_fuzz(H, torch_mod, oracle, family):
+    """One Nest per kernel family called (FUZZ_N or 30) times with random
+    sizes, ops, dtypes and pointer offsets in a row: the self-resetting
+    tickets, partial buffers and workspaces must leave every call exact
+    against the oracle (a stale ticket or partial shows as a wrong result)."""
+    from paper_2309_01906_b200 import nests
+    from tests.nestutil import oracle_levels
+    torch = torch_mod
+    rng = np.random.default_rng({"flat": 1, "hist": 2, "rowwise": 3, "teams": 4, "segrows": 5}[family] + 9000)
+    C, K, W = 5, 2, 4
+    levels = {"flat": nests.c5_nest(K), "hist": nests.c4_nest(K), "rowwise": nests.c2_nest(),
+              "teams": nests.c1_nest(outer=0), "segrows": nests.c3_fast_nest()}[family]
+    if family == "segrows":
+        W = 8
+    nest = H.Nest(levels, device=0, cluster_dim=K, warps_per_cta=W, clusters=C)  # one Nest for every call
+    for _ in range(FUZZ_N or 30):
+        if family == "flat":
+            n = int(rng.integers(0, 200000))
+            dt, op = [("f32", H.OP_SUM), ("i32", H.OP_MAX), ("f64", H.OP_SUM), ("i64", H.OP_AFFINE)][int(rng.integers(4))]
+            x = (gen.gen_f32(int(rng.integers(100)), 0, n) if dt == "f32" else gen.gen_i32(int(rng.integers(100)), 0, n)
+                 if dt == "i32" else rng.standard_normal(n) if dt == "f64" else rng.integers(-(1 << 62), 1 << 62, n))
+            mis = int(rng.integers(0, 16 // x.itemsize)) * x.itemsize if n else 0
+            res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis, coverage=False, partials=False, nest=nest)
+            compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W, partials=False)
+        elif family == "hist":
+            n = int(rng.integers(0, 300000))
+            x = gen.gen_u8_zipf(int(rng.integers(100)), 0, n)
+            mis = int(rng.integers(0, 16)) if n else 0
+            res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, misalign=mis, coverage=False,
+                           partials=False, nest=nest)
+            assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
+        elif family in ("rowwise", "teams"):
+            n0, n1 = int(rng.integers(1, 80)), int(rng.integers(1, 3000))
+            dt, op = [("f32", H.OP_SUM), ("i32", H.OP_MIN), ("f64", H.OP_MAX), ("i64", H.OP_AFFINE)][int(rng.integers(4))]
+            x = (gen.gen_f32(int(rng.integers(100)), 0, n0 * n1) if dt == "f32" else
+                 gen.gen_i32(int(rng.integers(100)), 0, n0 * n1) if dt == "i32" else
+                 rng.standard_normal(n0 * n1) if dt == "f64" else rng.integers(-(1 << 62), 1 << 62, n0 * n1))
+            keyed = family == "rowwise"
+            res = run_nest(H, torch, levels, x, n0=n0, n1=n1, keyed=keyed, op=op, C=C, K=K, W=W, coverage=False,
+                           partials=False, nest=nest)
+            compare(oracle, H, levels, res, x, n0=n0, n1=n1, keyed=keyed, op=op, C=C, K=K, W=W, partials=False)
+        else:
+            rows = int(rng.integers(1, 2000))
+            lens = np.where(rng.random(rows) < 0.01, rng.integers(4097, 20000, rows), rng.geometric(0.1, rows))
+            off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+            v = rng.standard_normal(int(off[-1])) + 3.0  # no near-cancelling rows (the tolerance is relative)
+            res = run_nest(H, torch, levels, v, n0=rows, offsets=off, keyed=True, C=C, K=2, W=W, coverage=False,
+                           partials=False, nest=nest)
+            ol = oracle_levels(oracle, nests.c3_nest(with_gpu=False, rows_chunk=16, width=8), 1, 2, 2, 4)
+            assert_rel(res["out"], oracle.nest_run(ol, n0=rows, offsets=off, x=v, keyed=True, coverage=False,
+                                                   partials=False).result)
+        assert res["kernel"] != "generic", res["kernel"]
+
+
+def test_csr_n1_zero_reads_nnz(H, torch_mod, oracle):
+    """hpar.h lets a CSR call pass n1 = 0 (the value count is then read from
+    offsets[n0_local] on the device): both fused CSR kernels, with long rows
+    (> 4096, the chunk / segment lists sized from that count), vs the oracle;
+    and inside graph capture such a call is refused (HPAR_E_INVALID)."""
+    from paper_2309_01906_b200 import nests
+    from tests.nestutil import oracle_levels
+    torch = torch_mod
+    rng = np.random.default_rng(77)
+    rows = 3000
+    lens = np.where(rng.random(rows) < 0.01, rng.integers(4097, 30000, rows), rng.geometric(0.1, rows))
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    offd = torch.from_numpy(off).cuda()
+    nest = H.Nest(nests.c3_fast_nest(), device=0, cluster_dim=2, warps_per_cta=8, clusters=5)
+    v32 = gen.gen_f32(gen.SEED_C3, 0, int(off[-1]))
+    out = torch.full((rows,), -1.0, dtype=torch.float64, device="cuda")
+    nest.parallel_for_reduce(H.make_desc(torch.from_numpy(v32).cuda(), out, n0=rows, n1=0, nloops=2, keyed=True,
+                                         offsets=offd, out_dtype=H.F64))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "segmented_csr"
+    assert_rel(out.cpu().numpy(), oracle.segsum_f32(v32, off))
+    v = rng.standard_normal(int(off[-1])) + 3.0
+    out.fill_(-1.0)
+    nest.parallel_for_reduce(H.make_desc(torch.from_numpy(v).cuda(), out, n0=rows, n1=0, nloops=2, keyed=True,
+                                         offsets=offd, out_dtype=H.F64))
+    torch.cuda.synchronize()
+    assert nest.last_kernel() == "segrows_csr"
+    ol = oracle_levels(oracle, nests.c3_nest(with_gpu=False, rows_chunk=16, width=8), 1, 2, 2, 4)
+    assert_rel(out.cpu().numpy(), oracle.nest_run(ol, n0=rows, offsets=off, x=v, keyed=True, coverage=False,
+                                                  partials=False).result)
+    xd = torch.from_numpy(v32).cuda()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(H.HparError) as e:
+        with torch.cuda.graph(g, stream=s):
+            nest.parallel_for_reduce(H.make_desc(xd, out, n0=rows, n1=0, nloops=2, keyed=True, offsets=offd,
+                                                 out_dtype=H.F64), s.cuda_stream)
+    assert e.value.code == H.HPAR_E_INVALID
 
 
 def test_generic_min_max(H, torch_mod, oracle):
