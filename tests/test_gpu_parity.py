@@ -65,7 +65,8 @@ def test_device_generator_matches_numpy(inputs_lib, torch_mod):
 
 # ---------------------------------------------------------------------------
 def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, C=4, K=2, W=4,
-             partials=True, coverage=True, max_inner=0, out_f64=True, misalign=0, ld=0, nest=None):
+             partials=True, coverage=True, max_inner=0, out_f64=True, misalign=0, ld=0, nest=None,
+             fingerprint=False):
     if nest is None:  # (a caller may pass one Nest to reuse across calls)
         nest = H.Nest(levels, device=0, cluster_dim=K, warps_per_cta=W, clusters=C)
     nloops = 2 if (n1 or offsets is not None) else 1
@@ -123,15 +124,19 @@ def run_nest(H, torch, levels, x, *, n0, n1=0, offsets=None, keyed=False, op=0, 
                                     device="cuda"))
     offs = torch.from_numpy(offsets).cuda() if offsets is not None else None
     verify = (H.VERIFY_COVERAGE if coverage else 0) | (H.VERIFY_PARTIALS if partials else 0)
+    fpt = torch.zeros(3, dtype=torch.int64, device="cuda") if fingerprint else None
+    if fingerprint:
+        verify |= H.VERIFY_FINGERPRINT
     d = H.make_desc(xd, out, op=op, n0=n0, n1=n1, ld=ld or n1, nloops=nloops, keyed=keyed, offsets=offs,
-                    max_inner=max_inner, verify=verify, partials=parts, owner=owner, count=count,
+                    max_inner=max_inner, verify=verify, partials=parts, owner=owner, count=count, fingerprint=fpt,
                     out_dtype=(H.U64 if op == H.OP_AFFINE else (H.F64 if fp else H.I64)) if keyed else -1)
     nest.parallel_for_reduce(d)
     torch.cuda.synchronize()
     res = out.cpu().numpy()
     return dict(nest=nest, out=res, owner=owner.cpu().numpy()[:n_iter] if coverage else None,
                 count=count.cpu().numpy()[:n_iter] if coverage else None,
-                parts=[p.cpu().numpy() if p is not None else None for p in parts], kernel=nest.last_kernel())
+                parts=[p.cpu().numpy() if p is not None else None for p in parts], kernel=nest.last_kernel(),
+                fp=fpt.cpu().numpy().view(np.uint64) if fingerprint else None)
 
 
 def compare(oracle, H, levels, res, x, *, n0, n1=0, offsets=None, keyed=False, op=0, C, K, W,
@@ -1289,9 +1294,13 @@ def test_flat_fuzz(H, torch_mod, oracle, seed):
     else:
         levels += [H.Level(H.HPAR_WARP, H.HPAR_WARP, H.STATIC_CHUNK, chunk=32 * V),
                    H.Level(H.HPAR_LANE, H.HPAR_LANE, H.STATIC_CHUNK, chunk=V)]
-    res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis)
+    fpr = bool(rng.random() < 0.5)  # also the coverage fingerprints (F_once, F_owner, count) vs the oracle's
+    res = run_nest(H, torch, levels, x, n0=n, op=op, C=C, K=K, W=W, misalign=mis, fingerprint=fpr)
     assert res["kernel"] == "flat_tma", (n, tile, K, W, V, dt, spell)
     compare(oracle, H, levels, res, x, n0=n, op=op, C=C, K=K, W=W)
+    if fpr:
+        once, own = oracle.fp_flat_range(oracle_levels(oracle, levels, 1, C, K, W), n, 0, n)
+        assert (int(res["fp"][0]), int(res["fp"][1]), int(res["fp"][2])) == (once, own, n)
 
 
 @pytest.mark.parametrize("seed", range(FUZZ_N or 20))
@@ -1324,8 +1333,12 @@ def test_hist_fuzz(H, torch_mod, oracle, seed):
     else:
         levels += [H.Level(H.HPAR_WARP, H.HPAR_WARP, H.STATIC_CHUNK, chunk=512),
                    H.Level(H.HPAR_LANE, H.HPAR_LANE, H.STATIC_CHUNK, chunk=16)]
-    res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, misalign=mis)
+    fpr = bool(rng.random() < 0.5)  # also the coverage fingerprints vs the oracle's
+    res = run_nest(H, torch, levels, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W, misalign=mis, fingerprint=fpr)
     assert res["kernel"].startswith("hist256_lanepriv"), (n, tile, K, W, spell)
+    if fpr:
+        once, own = oracle.fp_flat_range(oracle_levels(oracle, levels, 1, C, K, W), n, 0, n)
+        assert (int(res["fp"][0]), int(res["fp"][1]), int(res["fp"][2])) == (once, own, n)
     assert np.array_equal(res["out"].astype(np.uint64), oracle.hist256(x))
     compare(oracle, H, levels, res, x, n0=n, op=H.OP_HIST256, C=C, K=K, W=W)
 
