@@ -235,3 +235,43 @@ def test_barrier_levels_host(H):
     with pytest.raises(H.HparError) as e:
         nest.barrier(H.HPAR_LANE)
     assert e.value.code == H.HPAR_E_INVALID and "describe-only" in str(e.value)
+
+
+def test_nest_validation_fuzz(H):
+    """Random level lists (slices of the hierarchy, schedules, chunks,
+    partitions, fanouts, loops, geometries) through hpar_nest_create on
+    describe-only nests: every call either succeeds with a consistent info
+    (per-level tasks = the product of the collapsed hardware counts, a lane
+    partition dividing 32) or fails with one of the model's error codes —
+    never another exception or a crash."""
+    import random
+    d = H.b200_desc()
+    rng = random.Random(4242)
+    codes = {H.HPAR_E_INVALID, H.HPAR_E_CAPABILITY, H.HPAR_E_SCHEDULE, H.HPAR_E_PARTITION, H.HPAR_E_UNSUPPORTED}
+    ok = 0
+    for _ in range(600):
+        cuts = sorted(rng.sample(range(2, 6), rng.randint(0, 4)))
+        first = rng.choice([1, 1, 1, 2, 3])
+        bounds = [first] + [c for c in cuts if c > first] + [6]
+        levels = []
+        for i in range(len(bounds) - 1):
+            sch = rng.choice([H.STATIC, H.STATIC_CHUNK, H.DYNAMIC, H.NONE])
+            chunk = rng.choice([0, 1, 3, 64]) if sch in (H.STATIC_CHUNK, H.DYNAMIC) else 0
+            lv = H.Level(bounds[i], bounds[i + 1] - 1, sch, loop=rng.choice([0, 0, 1]), chunk=chunk)
+            if rng.random() < 0.1:
+                lv.width = rng.choice([2, 3, 4, 8])
+            if rng.random() < 0.1:
+                lv.fanout = rng.choice([1, 7, 64, 1024])
+            levels.append(lv)
+        K, W = rng.choice([1, 2, 4, 8, 16]), rng.choice([1, 4, 8, 32, 33])
+        try:
+            nest = H.Nest(levels, device=-1, desc=d, cluster_dim=K, warps_per_cta=W, clusters=rng.choice([0, 1, 148]),
+                          nranks=rng.choice([1, 2, 8]), rank=0)
+        except H.HparError as e:
+            assert e.code in codes, (levels, e)
+            continue
+        info = nest.info()
+        assert info.nlevels == len(levels)
+        assert info.lane_width == 0 or 32 % max(info.lane_width, 1) == 0
+        ok += 1
+    assert ok > 20  # (most random lists violate some rule; those must fail cleanly)
