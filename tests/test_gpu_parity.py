@@ -401,6 +401,50 @@ def test_csr_n1_zero_reads_nnz(H, torch_mod, oracle):
     assert e.value.code == H.HPAR_E_INVALID
 
 
+def test_desc_validation_fuzz(H, torch_mod):
+    """Random malformed calls through hpar_parallel_for_reduce on real nests:
+    bad ops / dtypes / out dtypes, negative extents, NULL pointers, loop and
+    keyed mismatches, verify without its buffers.  Each must fail with one of
+    the model's error codes before any launch — never a crash — and the nest
+    must stay usable (a valid call afterwards is exact)."""
+    from paper_2309_01906_b200 import nests
+    torch = torch_mod
+    rng = np.random.default_rng(99)
+    nest = H.Nest(nests.c5_nest(2), device=0, cluster_dim=2, warps_per_cta=4, clusters=3)
+    x = torch.ones(1000, dtype=torch.float32, device="cuda")
+    out = torch.zeros(4, dtype=torch.float64, device="cuda")
+    codes = {H.HPAR_E_INVALID, H.HPAR_E_UNSUPPORTED, H.HPAR_E_CAPABILITY}
+    for _ in range(200):
+        d = H.make_desc(x, out, n0=1000)
+        k = int(rng.integers(9))
+        if k == 0:
+            d.op = int(rng.choice([-1, 5, 99]))
+        elif k == 1:
+            d.in_dtype = int(rng.choice([-1, 9]))
+        elif k == 2:
+            d.op = H.OP_HIST256  # u8 only
+        elif k == 3:
+            d.n0 = -int(rng.integers(1, 100))
+        elif k == 4:
+            d.out = None
+        elif k == 5:
+            d.nloops = int(rng.choice([0, 3]))
+        elif k == 6:
+            d.in_ = None
+        elif k == 7:
+            d.verify = H.VERIFY_COVERAGE  # no owner / count buffers
+        else:
+            d.op = H.OP_AFFINE  # int64 only
+        with pytest.raises(H.HparError) as e:
+            nest.parallel_for_reduce(d)
+        assert e.value.code in codes, (k, e.value)
+    torch.cuda.synchronize()
+    out.zero_()
+    nest.parallel_for_reduce(H.make_desc(x, out, n0=1000))
+    torch.cuda.synchronize()
+    assert out[0].item() == 1000.0
+
+
 def test_generic_min_max(H, torch_mod, oracle):
     torch = torch_mod
     levels = [H.Level(H.HPAR_CLUSTER, H.HPAR_CTA, 1, chunk=5), H.Level(H.HPAR_WARP, H.HPAR_LANE, 0)]
