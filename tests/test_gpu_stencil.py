@@ -165,3 +165,20 @@ def test_stencil_fuzz(env, seed):
     want[r0:r0 + nr, c0:c0 + nc] = G.stencil5(A, 1)[r0:r0 + nr, c0:c0 + nc]
     assert np.array_equal(got, want), (R, C, ld, r0, c0, nr, nc)
     assert (b.cpu().numpy()[:, C:] == -7.0).all(), "padding columns written"
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("HPAR_FUZZ_N", "0")) or 8))
+def test_mapped_siblings_fuzz(env, seed):
+    """Random sibling grids with a one-cell ghost ring (the §4 mapping
+    generalised: gy x gx siblings, ty x tx from-tiles, to = from + ring): T
+    sweeps, each followed by the ghost refresh between the siblings'
+    buffers, equal the sequential stencil over the whole array bit for bit."""
+    torch, H, nest = env
+    rng = np.random.default_rng(7500 + seed)
+    gy, gx = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+    ty, tx = int(rng.integers(1, 70)), int(rng.integers(1, 150))
+    sp = G.MapSpec((gy * ty + 2, gx * tx + 2), gy * gx, gx, (G.MapDim(ty, 0, ty + 2), G.MapDim(tx, 0, tx + 2)),
+                   (G.MapDim(ty, 1, ty), G.MapDim(tx, 1, tx)))
+    A = field(*sp.extent, seed=gen.SEED_C4 + seed)
+    T = int(rng.integers(1, 5))
+    assert np.array_equal(_mapped_on_one_gpu(torch, H, nest, sp, A, T), G.stencil5(A, T)), (gy, gx, ty, tx, T)
